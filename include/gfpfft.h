@@ -1,0 +1,150 @@
+/*
+ * gfpfft.h -- C-ABI of the B200-native GF(p) FFT library (libgfpfft.so),
+ * p = r^k + 1 a generalized Fermat prime, k a power of two, 2 <= r < 2^64.
+ *
+ * This is the drop-in boundary for the reference package `gfpfft`
+ * (arxiv/paper_1811_01490).  The reference is pure Python; its "plugin"
+ * surface is the field protocol consumed by fft.py (fft.py:13-17) and the
+ * public functions re-exported by gfpfft/__init__.py:9-38.  Each entry point
+ * below cites the reference function it replaces.  A reference-side binding
+ * (ctypes) is shown in INTEGRATION.md.
+ *
+ * Conventions
+ *   - Device buffers are digit-major: a vector of n elements is
+ *     uint64[k][n] (digit d of element i at ptr[d * n + i]); a batch of
+ *     transforms is uint64[batch][k][N].  All device pointers must be
+ *     8-byte aligned device memory.  Host entry points (*_host) take
+ *     element-major uint64[n][k] (the reference's tuple order and the GFPV
+ *     payload order, bench_cli.py:88-116).
+ *   - Inputs must be canonical (gfp_field.py:1-8: every digit < r, or the
+ *     form-B encoding (0,...,0,r) of p-1).  Outputs are canonical.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *     stream-ordered and asynchronous unless the name ends in _host.
+ *   - Return codes: GFP_OK, or an error the Python layer maps to the
+ *     reference's exception (ValueError / ConfigurationError).
+ */
+#ifndef GFPFFT_H
+#define GFPFFT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GFP_OK 0
+#define GFP_EINVAL 1      /* ValueError in the reference */
+#define GFP_ECONFIG 2     /* gfp_mult.ConfigurationError (gfp_mult.py:35) */
+#define GFP_ECUDA 3       /* CUDA runtime failure */
+#define GFP_ENOMEM 4      /* device allocation failure */
+#define GFP_EUNSUPPORTED 5 /* parameters outside the transform kernels' range */
+
+typedef struct gfp_fft_plan gfp_fft_plan;
+
+/* Human-readable message for a return code. */
+const char *gfp_strerror(int code);
+
+/* Library version (ABI revision). */
+int gfp_version(void);
+
+/* 1 if k*r^2 <= (P1*P2-1)/2 and 2k | P_i - 1 for the reference's default
+   word primes: check_prime_compat (gfp_mult.py:207-226).  The device
+   multiply does not need it (it is exact for every (k, r)); the Python
+   layer uses it to keep gfp_mul_fft's ConfigurationError contract. */
+int gfp_check_prime_compat(int k, uint64_t r);
+
+/* 1 if the transform / fast-multiply kernels accept (k, r): k in
+   {4, 8, 16, 32} and r large enough that the limb-split accumulation bounds
+   hold.  Every configuration in BASELINE.json qualifies. */
+int gfp_fast_path_ok(int k, uint64_t r);
+
+/* ---- element-wise vectors (device, digit-major [k][n]) ------------------ */
+
+/* z = x + y mod p.  Replaces gfp_add (gfp_field.py:82-109) per element. */
+int gfp_vec_add(const uint64_t *x, const uint64_t *y, uint64_t *z, int64_t n, int k,
+                uint64_t r, void *stream);
+
+/* z = x - y mod p.  Replaces gfp_sub (gfp_field.py:112-135). */
+int gfp_vec_sub(const uint64_t *x, const uint64_t *y, uint64_t *z, int64_t n, int k,
+                uint64_t r, void *stream);
+
+/* z = x * r^i mod p, 0 <= i <= 2k (GFP_EINVAL otherwise).  Replaces
+   gfp_mul_pow_r (gfp_field.py:138-161). */
+int gfp_vec_mul_pow_r(const uint64_t *x, uint64_t *z, int64_t n, int k, uint64_t r, int i,
+                      void *stream);
+
+/* z = x * y mod p, exact for every (k, r).  Replaces gfp_mul_fft
+   (gfp_mult.py:416-501) / gfp_mul_bigint (gfp_mult.py:504-512); both compute
+   the same canonical product.  y_inc = 1: element-wise; y_inc = 0: y is a
+   single element ([k][1]) broadcast over x. */
+int gfp_vec_mul(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z, int64_t n,
+                int k, uint64_t r, void *stream);
+
+/* z = x^e mod p, e given as little-endian host uint64 limbs shared by all
+   elements.  Replaces gfp_pow (gfp_field.py:164-177) /
+   GfpFftField.pow (gfp_mult.py:552-554). */
+int gfp_vec_pow(const uint64_t *x, const uint64_t *e_limbs, int e_nlimbs, uint64_t *z,
+                int64_t n, int k, uint64_t r, void *stream);
+
+/* out[i] = 1 if element i is canonical.  Replaces is_canonical
+   (gfp_field.py:49-56). */
+int gfp_vec_is_canonical(const uint64_t *x, uint8_t *out, int64_t n, int k, uint64_t r,
+                         void *stream);
+
+/* Seeded synthetic canonical elements, digits uniform in [0, r). */
+int gfp_vec_uniform(uint64_t *z, int64_t n, int k, uint64_t r, uint64_t seed, void *stream);
+
+/* Layout conversion element-major [n][k] <-> digit-major [k][n] (device). */
+int gfp_to_digit_major(const uint64_t *src, uint64_t *dst, int64_t n, int k, void *stream);
+int gfp_to_element_major(const uint64_t *src, uint64_t *dst, int64_t n, int k, void *stream);
+
+/* ---- transforms ----------------------------------------------------------- */
+
+/* Plan for the DFT of N = K^e points at root omega (host array of k
+   canonical digits).  Replaces build_plan (fft.py:237-275) for the GFP field
+   (GfpFftField, gfp_mult.py:518-592): validates omega^N = 1,
+   omega^(N/2) = -1, K = 2k and omega^(N/2k) in {r, 1/r} exactly like the
+   reference (GFP_EINVAL otherwise), and builds the device twiddle tables
+   (omega^j, j < N/K, and omega^j * N^-1) with the exact device multiply.
+   Work is enqueued on `stream`; the call synchronises it before returning. */
+int gfp_fft_plan_create(gfp_fft_plan **plan, int k, uint64_t r, int K, int e,
+                        const uint64_t *omega, void *stream);
+
+int gfp_fft_plan_destroy(gfp_fft_plan *plan);
+
+/* N of a plan, and the number of uint64 words of device workspace
+   gfp_fft_exec / gfp_poly_mul need for `batch` transforms. */
+int64_t gfp_fft_plan_size(const gfp_fft_plan *plan);
+int64_t gfp_fft_workspace_words(const gfp_fft_plan *plan, int64_t batch);
+
+/* Forward (inverse = 0) or inverse (inverse = 1, includes the N^-1 scale)
+   DFT of `batch` vectors, natural order in and out, digit-major
+   [batch][k][N].  in may equal out.  Replaces dft_general (fft.py:298-360)
+   and dft_inverse (fft.py:363-370). */
+int gfp_fft_exec(const gfp_fft_plan *plan, const uint64_t *in, uint64_t *out, uint64_t *work,
+                 int64_t batch, int inverse, void *stream);
+
+/* Cyclic product of length N: out = IDFT(DFT(f) .* DFT(g)), the polynomial
+   product when deg f + deg g < N (the reference composes
+   it from dft_general, GfpFftField.mul and dft_inverse). */
+int gfp_poly_mul(const gfp_fft_plan *plan, const uint64_t *f, const uint64_t *g,
+                 uint64_t *out, uint64_t *work, int64_t batch, void *stream);
+
+/* Host-buffer entry points (element-major [batch][N][k] host arrays; H2D,
+   transform, D2H; synchronous).  The call a reference-side binding makes
+   in place of dft_general / dft_inverse / the poly-mul composition on a
+   list of digit tuples. */
+int gfp_fft_exec_host(gfp_fft_plan *plan, uint64_t *v, int64_t batch, int inverse,
+                      void *stream);
+int gfp_poly_mul_host(gfp_fft_plan *plan, const uint64_t *f, const uint64_t *g, uint64_t *out,
+                      int64_t batch, void *stream);
+
+/* Number of kernel launches issued by the last exec/poly_mul call on this
+   plan (instrumentation for the benchmark's gpu_launches count). */
+int64_t gfp_fft_plan_last_launches(const gfp_fft_plan *plan);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GFPFFT_H */

@@ -1,0 +1,235 @@
+// gfp_device.cuh -- device arithmetic for GF(p), p = r^k + 1, radix-r digits.
+//
+// Element representation (reference: gfp_field.py:1-8): k little-endian
+// radix-r digits.  Canonical form A has every digit in [0, r); form B is
+// (0, ..., 0, r) = p - 1.  Device buffers are digit-major ([k][n] per
+// vector) so a warp reading one digit row of consecutive elements issues
+// fully coalesced loads.
+//
+// Two digit regimes are used on the device:
+//   * canonical  -- what every public entry point consumes and produces;
+//   * lazy       -- signed 64-bit digits in [-delta, r + delta] (delta tiny),
+//                   the carry-save form the transform keeps between passes so
+//                   butterflies are plain digit-wise adds with no carry chain.
+// Multiplication by r^a on any digit vector is exact as a rotation with the
+// wrapped digits negated, because r^k = -1, so shifts
+// never need normalisation.
+#pragma once
+#include <stdint.h>
+
+typedef uint64_t u64;
+typedef int64_t i64;
+typedef unsigned __int128 u128;
+typedef __int128 i128;
+
+#define GFP_HD __host__ __device__ __forceinline__
+#define GFP_D __device__ __forceinline__
+
+// Per-radix constants, computed once on the host (exact integer arithmetic in
+// the Python plan code) and passed by value to every kernel.
+struct RadixConsts {
+    u64 r;
+    u64 d_norm;     // r << sh (top bit set)
+    u64 v_recip;    // floor((2^128 - 1) / d_norm) - 2^64  (Moller-Granlund)
+    u64 bias_lo;    // 2^63 * r as a 128-bit constant (fast-multiply bias)
+    u64 bias_hi;
+    double rinv;    // 1.0 / r (quotient estimates for small quotients)
+    int sh;         // leading zeros of r
+    int s;          // limb split for the fast multiply: digit = hi * 2^s + lo
+    int stages_per_norm;  // lazy radix-2 stages allowed between normalisations
+    int pad;
+};
+
+// ---------------------------------------------------------------------------
+// 128-by-64 division with a precomputed reciprocal (Moller & Granlund,
+// "Improved division by invariant integers", Alg. 4).  d normalised, u1 < d.
+GFP_D u64 mg_div(u64 u1, u64 u0, u64 d, u64 v, u64 &rem)
+{
+    u64 q0 = v * u1;
+    u64 q1 = __umul64hi(v, u1);
+    u64 t = q0 + u0;
+    q1 = q1 + u1 + 1 + (t < q0 ? 1 : 0);
+    q0 = t;
+    u64 rr = u0 - q1 * d;
+    if (rr > q0) {
+        q1 -= 1;
+        rr += d;
+    }
+    if (rr >= d) {
+        q1 += 1;
+        rr -= d;
+    }
+    rem = rr;
+    return q1;
+}
+
+// (u1:u0) / r for u1 < r, any r >= 2.
+GFP_D u64 div128_by_r(u64 u1, u64 u0, const RadixConsts &rc, u64 &rem)
+{
+    int sh = rc.sh;
+    u64 n1 = sh ? ((u1 << sh) | (u0 >> (64 - sh))) : u1;
+    u64 n0 = u0 << sh;
+    u64 rn;
+    u64 q = mg_div(n1, n0, rc.d_norm, rc.v_recip, rn);
+    rem = rn >> sh;
+    return q;
+}
+
+// floor division of a signed 64-bit value whose quotient is small
+// (|v| / r < 2^50); returns q and sets rem in [0, r).
+GFP_D i64 floordiv_small(i64 v, const RadixConsts &rc, i64 &rem)
+{
+    double est = (double)v * rc.rinv;
+    i64 q = (i64)floor(est);
+    i64 rr = v - q * (i64)rc.r;
+    if (rr < 0) {
+        q -= 1;
+        rr += (i64)rc.r;
+    } else if (rr >= (i64)rc.r) {
+        q += 1;
+        rr -= (i64)rc.r;
+    }
+    rem = rr;
+    return q;
+}
+
+// ---------------------------------------------------------------------------
+// Canonical digit arithmetic, thread-serial, exact for any 2 <= r < 2^64.
+// These restate gfp_field.py:82-161 digit loop for digit loop, since they are
+// the element-wise public API (gfp_add / gfp_sub / gfp_mul_pow_r).
+
+template <typename Digits>
+GFP_HD void set_form_b(Digits &z, int k, u64 r)
+{
+    for (int i = 0; i < k; i++)
+        z[i] = 0;
+    z[k - 1] = r;
+}
+
+// gfp_add (gfp_field.py:82-109)
+template <typename DX, typename DY, typename DZ>
+GFP_HD void dev_gfp_add(const DX &x, const DY &y, DZ &z, int k, u64 r)
+{
+    u64 carry = 0;
+    for (int i = 0; i < k; i++) {
+        u64 a = x[i], b = y[i];
+        u64 s = a + b;
+        u64 c1 = s < a;
+        u64 s2 = s + carry;
+        c1 |= (s2 < s);
+        bool ge = c1 || s2 >= r;
+        z[i] = ge ? s2 - r : s2;
+        carry = ge ? 1 : 0;
+    }
+    if (carry) {
+        bool done = false;
+        for (int i = 0; i < k; i++) {
+            if (!done) {
+                if (z[i]) {
+                    z[i] -= 1;
+                    done = true;
+                } else {
+                    z[i] = r - 1;
+                }
+            }
+        }
+        if (!done)
+            set_form_b(z, k, r);
+    }
+}
+
+// gfp_sub (gfp_field.py:112-135)
+template <typename DX, typename DY, typename DZ>
+GFP_HD void dev_gfp_sub(const DX &x, const DY &y, DZ &z, int k, u64 r)
+{
+    u64 borrow = 0;
+    for (int i = 0; i < k; i++) {
+        u64 a = x[i], b = y[i];
+        u64 d = a - b;
+        u64 b1 = a < b;
+        u64 d2 = d - borrow;
+        b1 |= (d < borrow);
+        z[i] = b1 ? d2 + r : d2;
+        borrow = b1;
+    }
+    if (borrow) {
+        bool done = false;
+        for (int i = 0; i < k; i++) {
+            if (!done) {
+                if (r >= 1 && z[i] < r - 1) {
+                    z[i] += 1;
+                    done = true;
+                } else {
+                    z[i] = 0;
+                }
+            }
+        }
+        if (!done)
+            set_form_b(z, k, r);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Canonicalisation of a digit vector with digits in [0, r) and a signed
+// overflow carry C (value = D + C * r^k = D - C mod p), |C| <= 1.
+template <typename DZ>
+GFP_HD void finish_canonical(DZ &z, int k, u64 r, int C)
+{
+    if (C == 1) {
+        // D - 1; D == 0 -> p - 1 (form B)
+        bool done = false;
+        for (int i = 0; i < k; i++) {
+            if (!done) {
+                if (z[i]) {
+                    z[i] -= 1;
+                    done = true;
+                } else {
+                    z[i] = r - 1;
+                }
+            }
+        }
+        if (!done)
+            set_form_b(z, k, r);
+    } else if (C == -1) {
+        // D + 1; D == r^k - 1 -> r^k = p - 1 (form B)
+        bool done = false;
+        for (int i = 0; i < k; i++) {
+            if (!done) {
+                if (z[i] < r - 1) {
+                    z[i] += 1;
+                    done = true;
+                } else {
+                    z[i] = 0;
+                }
+            }
+        }
+        if (!done)
+            set_form_b(z, k, r);
+    }
+}
+
+// Lazy digits (signed, |f_i - r/2| well below 2^62, |carry| small relative
+// to r) to canonical.  Exact; loops until the wrap carry is in {-1, 0, 1}.
+template <typename DF, typename DZ>
+GFP_D void lazy_to_canonical(const DF &f, DZ &z, int k, const RadixConsts &rc)
+{
+    i64 C = 0;
+    for (int i = 0; i < k; i++) {
+        i64 rem;
+        i64 q = floordiv_small((i64)f[i] + C, rc, rem);
+        z[i] = (u64)rem;
+        C = q;
+    }
+    // value = D + C r^k = D - C (mod p)
+    while (C > 1 || C < -1) {
+        i64 carry = -C;
+        for (int i = 0; i < k; i++) {
+            i64 rem;
+            i64 q = floordiv_small((i64)z[i] + carry, rc, rem);
+            z[i] = (u64)rem;
+            carry = q;
+        }
+        C = carry;
+    }
+    finish_canonical(z, k, rc.r, (int)C);
+}

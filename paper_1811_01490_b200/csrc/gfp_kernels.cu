@@ -1,0 +1,1157 @@
+// gfp_kernels.cu -- sm_100a kernels and the C-ABI of libgfpfft.so.
+//
+// Layout: digit-major device vectors ([k][n], [batch][k][N]); see
+// include/gfpfft.h and DESIGN.md.  Two kernel families:
+//
+//   element-wise (thread per element, any power-of-two k <= 128, any r):
+//     k_add / k_sub / k_mul_pow_r  restate gfp_field.py:82-161 digit loops;
+//     k_mul / k_pow                exact generic multiply (gfp_generic.cuh);
+//     k_mul_fast                   limb-split IMAD.WIDE multiply when eligible.
+//
+//   transform (k in {4, 8, 16, 32}, K = 2k):
+//     k_pass  one radix-K Stockham pass: coalesced digit-row loads, the
+//             general twiddle (or pointwise / N^-1) multiply in registers,
+//             the r^a part of the twiddle folded into the shared-memory store
+//             as a digit rotation, the K-point DFT at root r (or 1/r) as
+//             lazy radix-2 butterflies with one digit per lane (rotations by
+//             r^t are warp shuffles + sign flips), and the store in natural
+//             Stockham order.  The last pass canonicalises.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "gfp_device.cuh"
+#include "gfp_fast.cuh"
+#include "gfp_generic.cuh"
+#include "gfpfft.h"
+
+#define FULL_MASK 0xffffffffu
+
+// ===========================================================================
+// host-side constants
+// ===========================================================================
+
+static int ilog2_exact(int64_t v)
+{
+    int l = 0;
+    while (((int64_t)1 << l) < v)
+        l++;
+    return ((int64_t)1 << l) == v ? l : -1;
+}
+
+static bool valid_k(int k) { return k >= 1 && k <= 128 && (k & (k - 1)) == 0; }
+
+// Fast-path (limb split) bound check; exact integer arithmetic.  Returns
+// true and fills s / stages when every accumulation bound of fast_mul_lazy
+// and the lazy butterflies holds for digits in [-delta, r + delta].
+static bool fast_bounds(int k, u64 r, int *s_out, int *stages_out)
+{
+    if (!(k == 4 || k == 8 || k == 16 || k == 32))
+        return false;
+    if (r < ((u64)1 << 24) || r >= ((u64)1 << 62))
+        return false;
+    const u128 two63 = (u128)1 << 63;
+    int K = 2 * k;
+    int logK = ilog2_exact(K);
+    // stages between normalisations: 2^S (r + delta) < 2^62 with delta = 2^S + k + 8
+    int S = 0;
+    for (int t = 1; t <= logK; t++) {
+        u128 delta = ((u128)1 << t) + (u64)k + 8;
+        if ((((u128)r + delta) << t) < ((u128)1 << 62))
+            S = t;
+    }
+    if (S < 1)
+        return false;
+    u128 delta = ((u128)1 << S) + (u64)k + 8;
+    u128 X = (u128)r + delta;  // |lazy digit| bound
+    u128 Y = X;
+    for (int s = 31; s >= 20; s--) {
+        u128 L = ((u128)1 << s) - 1;
+        u128 Xh = (X >> s) + 1;
+        u128 Yh = (Y >> s) + 1;
+        if (Xh >= ((u128)1 << 31) || Yh >= ((u128)1 << 31))
+            continue;
+        u128 kk = (u128)k;
+        if (kk * L * L >= two63 || kk * L * Yh >= two63 || kk * Xh * L >= two63 ||
+            kk * Xh * Yh >= two63)
+            continue;
+        // |c| <= k X Y must satisfy k X Y < 2^63 r (bias keeps c + 2^63 r in [0, 2^64 r))
+        // compare k X Y / r < 2^63 without overflow: X, Y < 2^62 so X*Y < 2^124
+        u128 XY = X * Y;
+        u128 qmax = (XY / r) * kk + kk;  // |q| bound after the first division
+        if (qmax >= two63)
+            continue;
+        // second round input |e| <= r + qmax < 2^63
+        if ((u128)r + qmax + 2 >= two63)
+            continue;
+        // output delta' = (r + qmax) / r + 2 must be <= delta
+        u128 d2 = ((u128)r + qmax) / r + 2;
+        if (d2 > delta)
+            continue;
+        *s_out = s;
+        *stages_out = S;
+        return true;
+    }
+    return false;
+}
+
+static RadixConsts make_consts(int k, u64 r)
+{
+    RadixConsts c;
+    memset(&c, 0, sizeof(c));
+    c.r = r;
+    c.sh = __builtin_clzll(r);
+    c.d_norm = r << c.sh;
+    u128 all = ~(u128)0;
+    u128 v = all / c.d_norm;
+    c.v_recip = (u64)(v - ((u128)1 << 64));
+    u128 bias = (u128)r << 63;
+    c.bias_lo = (u64)bias;
+    c.bias_hi = (u64)(bias >> 64);
+    c.rinv = 1.0 / (double)r;
+    int s = 0, S = 0;
+    if (fast_bounds(k, r, &s, &S)) {
+        c.s = s;
+        c.stages_per_norm = S;
+    } else {
+        c.s = 0;
+        c.stages_per_norm = 0;
+    }
+    return c;
+}
+
+// ===========================================================================
+// element-wise kernels (grid-stride, thread per element)
+// ===========================================================================
+
+template <int KD>
+__global__ void k_add(const u64 *__restrict__ x, const u64 *__restrict__ y, u64 *__restrict__ z,
+                      int64_t n, u64 r, int sub)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        u64 a[KD], b[KD], c[KD];
+#pragma unroll
+        for (int d = 0; d < KD; d++) {
+            a[d] = x[d * n + i];
+            b[d] = y[d * n + i];
+        }
+        if (sub)
+            dev_gfp_sub(a, b, c, KD, r);
+        else
+            dev_gfp_add(a, b, c, KD, r);
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            z[d * n + i] = c[d];
+    }
+}
+
+// gfp_mul_pow_r (gfp_field.py:138-161): i >= k negates first, then
+// B - A with B the up-shifted digits, A the wrapped top digits; a form-B
+// digit r moves one slot up.
+template <int KD>
+__global__ void k_mul_pow_r(const u64 *__restrict__ x, u64 *__restrict__ z, int64_t n, u64 r,
+                            int shift)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        u64 a[KD], A[KD], B[KD];
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            a[d] = x[d * n + i];
+        int s = shift % (2 * KD);
+        if (s >= KD) {
+            u64 zero[KD];
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                zero[d] = 0;
+            dev_gfp_sub(zero, a, a, KD, r);
+            s -= KD;
+        }
+        if (s) {
+            bool formb = a[KD - 1] == r;
+#pragma unroll
+            for (int d = 0; d < KD; d++) {
+                int src = d - s;
+                B[d] = src >= 0 ? a[src] : 0;
+                A[d] = src < 0 ? a[src + KD] : 0;
+            }
+            if (formb) {
+                // a[k-1] = r lands in A[s-1]; carry it one slot up
+                for (int d = 0; d < KD; d++) {
+                    if (d == s - 1)
+                        A[d] -= r;
+                    if (d == s)
+                        A[d] += 1;
+                }
+            }
+            dev_gfp_sub(B, A, a, KD, r);
+        }
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            z[d * n + i] = a[d];
+    }
+}
+
+template <int KD>
+__global__ void k_mul_generic(const u64 *__restrict__ x, const u64 *__restrict__ y, int64_t y_inc,
+                              u64 *__restrict__ z, int64_t n, RadixConsts rc)
+{
+    int64_t yn = y_inc ? n : 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        u64 a[KD], b[KD], c[KD];
+        int64_t iy = y_inc ? i : 0;
+        for (int d = 0; d < KD; d++) {
+            a[d] = x[d * n + i];
+            b[d] = y[d * yn + iy];
+        }
+        gfp_mul_generic<KD>(a, b, c, rc);
+        for (int d = 0; d < KD; d++)
+            z[d * n + i] = c[d];
+    }
+}
+
+template <int KD>
+__global__ void k_mul_fast(const u64 *__restrict__ x, const u64 *__restrict__ y, int64_t y_inc,
+                           u64 *__restrict__ z, int64_t n, RadixConsts rc)
+{
+    int64_t yn = y_inc ? n : 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        i64 a[KD], b[KD], f[KD];
+        u64 c[KD];
+        int64_t iy = y_inc ? i : 0;
+#pragma unroll
+        for (int d = 0; d < KD; d++) {
+            a[d] = (i64)x[d * n + i];
+            b[d] = (i64)y[d * yn + iy];
+        }
+        fast_mul_lazy<KD>(a, b, f, rc);
+        lazy_to_canonical(f, c, KD, rc);
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            z[d * n + i] = c[d];
+    }
+}
+
+template <int KD>
+__global__ void k_pow(const u64 *__restrict__ x, const u64 *__restrict__ e, int nbits,
+                      u64 *__restrict__ z, int64_t n, RadixConsts rc)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        u64 a[KD], c[KD];
+        for (int d = 0; d < KD; d++)
+            a[d] = x[d * n + i];
+        gfp_pow_generic<KD>(a, e, nbits, c, rc);
+        for (int d = 0; d < KD; d++)
+            z[d * n + i] = c[d];
+    }
+}
+
+__global__ void k_is_canonical(const u64 *__restrict__ x, uint8_t *__restrict__ out, int64_t n,
+                               int k, u64 r)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        bool all = true, lowzero = true;
+        for (int d = 0; d < k; d++) {
+            u64 v = x[d * n + i];
+            if (v >= r)
+                all = false;
+            if (d < k - 1 && v)
+                lowzero = false;
+        }
+        out[i] = (all || (lowzero && x[(int64_t)(k - 1) * n + i] == r)) ? 1 : 0;
+    }
+}
+
+GFP_D u64 splitmix64(u64 z)
+{
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_uniform(u64 *__restrict__ z, int64_t n, int k, u64 r, u64 seed)
+{
+    int64_t total = n * k;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        u64 h = splitmix64(seed * 0x2545F4914F6CDD1DULL + (u64)t);
+        z[t] = __umul64hi(h, r);  // uniform in [0, r)
+    }
+}
+
+// element-major [n][k] -> digit-major [k][n] (dir = 0) or back (dir = 1)
+__global__ void k_transpose(const u64 *__restrict__ src, u64 *__restrict__ dst, int64_t n, int k,
+                            int dir)
+{
+    int64_t total = n * k;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        // t indexes the destination linearly for coalesced stores
+        if (dir == 0) {
+            int64_t d = t / n, i = t % n;
+            dst[t] = src[i * k + d];
+        } else {
+            int64_t i = t / k, d = t % k;
+            dst[t] = src[d * n + i];
+        }
+    }
+}
+
+// ===========================================================================
+// transform pass kernel
+// ===========================================================================
+
+struct PassArgs {
+    const u64 *in;
+    u64 *out;
+    const u64 *table;  // element-major [M][k] canonical, omega^b (or omega^b / N)
+    const u64 *pre;    // optional pointwise operand, digit-major like `in`
+    int64_t N, M, Ns;
+    int64_t batch_stride;
+    int neg_exp;   // twiddle exponent N - E (inverse transform)
+    int rot_inv;   // base-case root of this execution is 1/r (rotations by r^-t)
+    int root_inv;  // the plan's omega^M is 1/r (twiddle split r^-a omega^b)
+    int scale;     // every element gets a table multiply (N^-1 folded in)
+    int canon;     // canonical output (last pass)
+    RadixConsts rc;
+};
+
+template <int KD>
+GFP_D i64 rot_lane(i64 val, int t, int d, bool inverse)
+{
+    // multiply the digit vector held one-digit-per-lane by r^t (forward) or
+    // r^-t (inverse), 0 < t < k: a rotation with the wrapped digits negated
+    int src = inverse ? ((d + t) & (KD - 1)) : ((d - t) & (KD - 1));
+    i64 v = __shfl_sync(FULL_MASK, val, src, KD);
+    bool neg = inverse ? (d + t >= KD) : (d < t);
+    return neg ? -v : v;
+}
+
+template <int KD>
+GFP_D void normalize_lane(i64 &v, int d, const RadixConsts &rc)
+{
+    i64 rem;
+    i64 q = floordiv_small(v, rc, rem);
+    int qi = (int)q;
+    int qin = __shfl_sync(FULL_MASK, qi, (d - 1) & (KD - 1), KD);
+    v = rem + (d == 0 ? -(i64)qin : (i64)qin);
+}
+
+template <int K>
+__host__ __device__ constexpr int bitrev_c(int x)
+{
+    int y = 0;
+    for (int b = 1; b < K; b <<= 1) {
+        y = (y << 1) | (x & 1);
+        x >>= 1;
+    }
+    return y;
+}
+
+template <int KD>
+__global__ void __launch_bounds__(256) k_pass(PassArgs A)
+{
+    constexpr int K = 2 * KD;
+    constexpr int ROW = KD + 1;  // padded smem row (bank spread)
+    extern __shared__ i64 sm[];  // [K][G][ROW]
+    const int G = blockDim.x / KD;
+    const int tid = threadIdx.x;
+    const int64_t bidx = blockIdx.y;
+    const int64_t j0 = (int64_t)blockIdx.x * G;
+    const int64_t N = A.N, M = A.M, Ns = A.Ns;
+    const u64 *in = A.in + bidx * A.batch_stride;
+    u64 *out = A.out + bidx * A.batch_stride;
+    const u64 *pre = A.pre ? A.pre + bidx * A.batch_stride : nullptr;
+    const RadixConsts rc = A.rc;
+
+    // ---- phase A: load K elements per group, twiddle / pointwise multiply
+#pragma unroll 1
+    for (int h = 0; h < 2; h++) {
+        const int g = tid % G;
+        const int t = tid / G + h * KD;
+        const int64_t j = j0 + g;
+        i64 x[KD];
+        int a = 0;
+        if (j < M) {
+            const int64_t pos = j + (int64_t)t * M;
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                x[d] = (i64)__ldg(in + d * N + pos);
+            if (pre) {
+                i64 y[KD];
+#pragma unroll
+                for (int d = 0; d < KD; d++)
+                    y[d] = (i64)__ldg(pre + d * N + pos);
+                fast_mul_lazy<KD>(x, y, x, rc);
+            }
+            int64_t E = 0;
+            if (Ns > 1)
+                E = (int64_t)t * (j % Ns) * (M / Ns);
+            if (A.neg_exp && E)
+                E = N - E;
+            a = (int)(E / M);
+            const int64_t b = E - (int64_t)a * M;
+            // omega^M is r (or 1/r for plans built on an inverse root)
+            if (A.root_inv && a)
+                a = 2 * KD - a;
+            if (b || A.scale) {
+                i64 y[KD];
+                const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(A.table + b * KD);
+#pragma unroll
+                for (int d = 0; d < KD; d += 2) {
+                    ulonglong2 w = __ldg(tp + d / 2);
+                    y[d] = (i64)w.x;
+                    y[d + 1] = (i64)w.y;
+                }
+                fast_mul_lazy<KD>(x, y, x, rc);
+            }
+        } else {
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                x[d] = 0;
+        }
+        // x * r^a: rotation by a (0 <= a < 2k), wrapped digits negated
+        i64 *row = sm + ((int64_t)t * G + g) * ROW;
+#pragma unroll
+        for (int d = 0; d < KD; d++) {
+            int p = d + a;
+            i64 v = x[d];
+            if (p >= KD) {
+                p -= KD;
+                v = -v;
+            }
+            if (p >= KD) {
+                p -= KD;
+                v = -v;
+            }
+            row[p] = v;
+        }
+    }
+    __syncthreads();
+
+    // ---- phase B: K-point DFT at root r (or 1/r), one digit per lane
+    {
+        const int d = tid % KD;
+        const int g = tid / KD;
+        const bool inv = A.rot_inv != 0;
+        i64 v[K];
+#pragma unroll
+        for (int t = 0; t < K; t++)
+            v[t] = sm[((int64_t)t * G + g) * ROW + d];
+        const int S = rc.stages_per_norm;
+        int stage = 0;
+#pragma unroll
+        for (int len = K / 2; len >= 1; len >>= 1) {
+#pragma unroll
+            for (int st = 0; st < K; st += 2 * len) {
+#pragma unroll
+                for (int i = 0; i < len; i++) {
+                    i64 a0 = v[st + i], b0 = v[st + i + len];
+                    v[st + i] = a0 + b0;
+                    i64 df = a0 - b0;
+                    const int tw = i * (K / (2 * len));  // exponent of the root, < k
+                    v[st + i + len] = tw ? rot_lane<KD>(df, tw, d, inv) : df;
+                }
+            }
+            stage++;
+            if (len > 1 && stage % S == 0) {
+#pragma unroll
+                for (int t = 0; t < K; t++)
+                    normalize_lane<KD>(v[t], d, rc);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < K; t++)
+            normalize_lane<KD>(v[t], d, rc);
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < K; t++)
+            sm[((int64_t)bitrev_c<K>(t) * G + g) * ROW + d] = v[t];
+    }
+    __syncthreads();
+
+    // ---- phase C: store in Stockham order (canonicalise on the last pass)
+#pragma unroll 1
+    for (int h = 0; h < 2; h++) {
+        const int g = tid % G;
+        const int u = tid / G + h * KD;
+        const int64_t j = j0 + g;
+        if (j >= M)
+            continue;
+        const int64_t pos = (j / Ns) * Ns * K + (j % Ns) + (int64_t)u * Ns;
+        const i64 *row = sm + ((int64_t)u * G + g) * ROW;
+        if (A.canon) {
+            i64 f[KD];
+            u64 c[KD];
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                f[d] = row[d];
+            lazy_to_canonical(f, c, KD, rc);
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                out[d * N + pos] = c[d];
+        } else {
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                out[d * N + pos] = (u64)row[d];
+        }
+    }
+}
+
+// power table: out[b] = omega^(b * step) for b < n, element-major [n][k]
+// (one thread per entry, square-and-multiply over the bits of b with the
+// precomputed omega^(2^i step) in `sq`), exact generic multiply.
+template <int KD>
+__global__ void k_power_table(const u64 *__restrict__ sq, int nsq, u64 *__restrict__ out,
+                              int64_t n, RadixConsts rc)
+{
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        u64 acc[KD];
+        for (int d = 0; d < KD; d++)
+            acc[d] = d == 0 ? 1 : 0;
+        for (int i = 0; i < nsq; i++) {
+            if ((b >> i) & 1) {
+                u64 y[KD];
+                for (int d = 0; d < KD; d++)
+                    y[d] = sq[(int64_t)i * KD + d];
+                gfp_mul_generic<KD>(acc, y, acc, rc);
+            }
+        }
+        for (int d = 0; d < KD; d++)
+            out[b * KD + d] = acc[d];
+    }
+}
+
+// sq[i] = omega^(2^i), element-major, single thread (plan time only)
+template <int KD>
+__global__ void k_squarings(const u64 *__restrict__ omega, u64 *__restrict__ sq, int nsq,
+                            RadixConsts rc)
+{
+    if (blockIdx.x || threadIdx.x)
+        return;
+    u64 cur[KD];
+    for (int d = 0; d < KD; d++)
+        cur[d] = omega[d];
+    for (int i = 0; i < nsq; i++) {
+        for (int d = 0; d < KD; d++)
+            sq[(int64_t)i * KD + d] = cur[d];
+        gfp_mul_generic<KD>(cur, cur, cur, rc);
+    }
+}
+
+// element-major table times a constant (element-major [1][k])
+template <int KD>
+__global__ void k_table_scale(const u64 *__restrict__ tab, const u64 *__restrict__ c,
+                              u64 *__restrict__ out, int64_t n, RadixConsts rc)
+{
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        u64 a[KD], y[KD], z[KD];
+        for (int d = 0; d < KD; d++) {
+            a[d] = tab[b * KD + d];
+            y[d] = c[d];
+        }
+        gfp_mul_generic<KD>(a, y, z, rc);
+        for (int d = 0; d < KD; d++)
+            out[b * KD + d] = z[d];
+    }
+}
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+
+static int g_num_sms = 0;
+
+static int num_sms()
+{
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0)
+            g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+static dim3 grid_for(int64_t work, int threads)
+{
+    int64_t blocks = (work + threads - 1) / threads;
+    int64_t cap = (int64_t)num_sms() * 32;
+    if (blocks > cap)
+        blocks = cap;
+    if (blocks < 1)
+        blocks = 1;
+    return dim3((unsigned)blocks);
+}
+
+static int cuda_status()
+{
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? GFP_OK : GFP_ECUDA;
+}
+
+#define DISPATCH_K(k, CALL)                                                                     \
+    switch (k) {                                                                                \
+    case 1: { constexpr int KD = 1; CALL; } break;                                              \
+    case 2: { constexpr int KD = 2; CALL; } break;                                              \
+    case 4: { constexpr int KD = 4; CALL; } break;                                              \
+    case 8: { constexpr int KD = 8; CALL; } break;                                              \
+    case 16: { constexpr int KD = 16; CALL; } break;                                            \
+    case 32: { constexpr int KD = 32; CALL; } break;                                            \
+    case 64: { constexpr int KD = 64; CALL; } break;                                            \
+    case 128: { constexpr int KD = 128; CALL; } break;                                          \
+    default: return GFP_EINVAL;                                                                 \
+    }
+
+#define DISPATCH_FAST_K(k, CALL)                                                                \
+    switch (k) {                                                                                \
+    case 4: { constexpr int KD = 4; CALL; } break;                                              \
+    case 8: { constexpr int KD = 8; CALL; } break;                                              \
+    case 16: { constexpr int KD = 16; CALL; } break;                                            \
+    case 32: { constexpr int KD = 32; CALL; } break;                                            \
+    default: return GFP_EUNSUPPORTED;                                                           \
+    }
+
+extern "C" {
+
+const char *gfp_strerror(int code)
+{
+    switch (code) {
+    case GFP_OK: return "ok";
+    case GFP_EINVAL: return "invalid argument";
+    case GFP_ECONFIG: return "configuration not supported by the prime pair";
+    case GFP_ECUDA: return "CUDA runtime error";
+    case GFP_ENOMEM: return "device allocation failed";
+    case GFP_EUNSUPPORTED: return "parameters outside the transform kernels' range";
+    default: return "unknown error";
+    }
+}
+
+int gfp_version(void) { return 1; }
+
+int gfp_check_prime_compat(int k, uint64_t r)
+{
+    const u64 P1 = 4179340454199820289ULL, P2 = 2485986994308513793ULL;
+    if (!valid_k(k) || r < 2)
+        return 0;
+    u128 limit = ((u128)P1 * P2 - 1) / 2;
+    u128 r2 = (u128)r * r;
+    if (r2 > limit / (u64)k)
+        return 0;
+    if ((P1 - 1) % (2 * (u64)k) || (P2 - 1) % (2 * (u64)k))
+        return 0;
+    return 1;
+}
+
+int gfp_fast_path_ok(int k, uint64_t r)
+{
+    int s, S;
+    return fast_bounds(k, r, &s, &S) ? 1 : 0;
+}
+
+static int check_kr(int k, u64 r)
+{
+    if (!valid_k(k) || r < 2)
+        return GFP_EINVAL;
+    return GFP_OK;
+}
+
+int gfp_vec_add(const uint64_t *x, const uint64_t *y, uint64_t *z, int64_t n, int k, uint64_t r,
+                void *stream)
+{
+    int e = check_kr(k, r);
+    if (e || n <= 0)
+        return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    DISPATCH_K(k, (k_add<KD><<<grid_for(n, 256), 256, 0, st>>>(x, y, z, n, r, 0)));
+    return cuda_status();
+}
+
+int gfp_vec_sub(const uint64_t *x, const uint64_t *y, uint64_t *z, int64_t n, int k, uint64_t r,
+                void *stream)
+{
+    int e = check_kr(k, r);
+    if (e || n <= 0)
+        return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    DISPATCH_K(k, (k_add<KD><<<grid_for(n, 256), 256, 0, st>>>(x, y, z, n, r, 1)));
+    return cuda_status();
+}
+
+int gfp_vec_mul_pow_r(const uint64_t *x, uint64_t *z, int64_t n, int k, uint64_t r, int i,
+                      void *stream)
+{
+    int e = check_kr(k, r);
+    if (e)
+        return e;
+    if (i < 0 || i > 2 * k)
+        return GFP_EINVAL;
+    if (n <= 0)
+        return GFP_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    DISPATCH_K(k, (k_mul_pow_r<KD><<<grid_for(n, 256), 256, 0, st>>>(x, z, n, r, i)));
+    return cuda_status();
+}
+
+int gfp_vec_mul(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z, int64_t n,
+                int k, uint64_t r, void *stream)
+{
+    int e = check_kr(k, r);
+    if (e || n <= 0)
+        return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    RadixConsts rc = make_consts(k, r);
+    if (rc.stages_per_norm > 0) {
+        DISPATCH_FAST_K(k, (k_mul_fast<KD><<<grid_for(n, 128), 128, 0, st>>>(x, y, y_inc, z, n,
+                                                                             rc)));
+    } else {
+        DISPATCH_K(k, (k_mul_generic<KD><<<grid_for(n, 128), 128, 0, st>>>(x, y, y_inc, z, n,
+                                                                           rc)));
+    }
+    return cuda_status();
+}
+
+int gfp_vec_pow(const uint64_t *x, const uint64_t *e_limbs, int e_nlimbs, uint64_t *z, int64_t n,
+                int k, uint64_t r, void *stream)
+{
+    int e = check_kr(k, r);
+    if (e)
+        return e;
+    if (n <= 0)
+        return GFP_OK;
+    if (e_nlimbs < 0)
+        return GFP_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    int nl = e_nlimbs > 0 ? e_nlimbs : 1;
+    u64 *d_e = nullptr;
+    if (cudaMallocAsync(&d_e, sizeof(u64) * nl, st) != cudaSuccess)
+        return GFP_ENOMEM;
+    u64 zero = 0;
+    cudaMemcpyAsync(d_e, e_nlimbs ? e_limbs : &zero, sizeof(u64) * nl, cudaMemcpyHostToDevice, st);
+    int nbits = 0;
+    for (int i = e_nlimbs - 1; i >= 0; i--)
+        if (e_limbs[i]) {
+            nbits = 64 * i + 64 - __builtin_clzll(e_limbs[i]);
+            break;
+        }
+    RadixConsts rc = make_consts(k, r);
+    DISPATCH_K(k, (k_pow<KD><<<grid_for(n, 64), 64, 0, st>>>(x, d_e, nbits, z, n, rc)));
+    int rcode = cuda_status();
+    cudaStreamSynchronize(st);  // e_limbs is caller host memory
+    cudaFreeAsync(d_e, st);
+    return rcode;
+}
+
+int gfp_vec_is_canonical(const uint64_t *x, uint8_t *out, int64_t n, int k, uint64_t r,
+                         void *stream)
+{
+    int e = check_kr(k, r);
+    if (e || n <= 0)
+        return e;
+    k_is_canonical<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, out, n, k, r);
+    return cuda_status();
+}
+
+int gfp_vec_uniform(uint64_t *z, int64_t n, int k, uint64_t r, uint64_t seed, void *stream)
+{
+    int e = check_kr(k, r);
+    if (e || n <= 0)
+        return e;
+    k_uniform<<<grid_for(n * k, 256), 256, 0, (cudaStream_t)stream>>>(z, n, k, r, seed);
+    return cuda_status();
+}
+
+int gfp_to_digit_major(const uint64_t *src, uint64_t *dst, int64_t n, int k, void *stream)
+{
+    if (!valid_k(k))
+        return GFP_EINVAL;
+    if (n <= 0)
+        return GFP_OK;
+    k_transpose<<<grid_for(n * k, 256), 256, 0, (cudaStream_t)stream>>>(src, dst, n, k, 0);
+    return cuda_status();
+}
+
+int gfp_to_element_major(const uint64_t *src, uint64_t *dst, int64_t n, int k, void *stream)
+{
+    if (!valid_k(k))
+        return GFP_EINVAL;
+    if (n <= 0)
+        return GFP_OK;
+    k_transpose<<<grid_for(n * k, 256), 256, 0, (cudaStream_t)stream>>>(src, dst, n, k, 1);
+    return cuda_status();
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// plans
+
+struct gfp_fft_plan {
+    int k, K, e;
+    int64_t N, M;
+    u64 r;
+    RadixConsts rc;
+    u64 *table;       // element-major [M][k]: omega^b
+    u64 *table_ninv;  // element-major [M][k]: omega^b * N^-1
+    // host-path scratch
+    u64 *h_dev;
+    int64_t h_words;
+    int64_t last_launches;
+    int root_inv;  // omega^(N/2k) == 1/r (a plan built on an inverse root)
+};
+
+static int pass_threads(int k, int64_t M, int *G_out)
+{
+    // groups per CTA: as many as fit 256 threads, fewer when the transform
+    // is too small to give every SM two CTAs
+    int Gmax = 256 / k;
+    int Gmin = 32 / k > 0 ? 32 / k : 1;
+    int G = Gmax;
+    while (G > Gmin && (M + G - 1) / G < 2 * (int64_t)num_sms())
+        G >>= 1;
+    *G_out = G;
+    return G * k;
+}
+
+template <int KD>
+static size_t pass_smem(int G)
+{
+    return (size_t)(2 * KD) * G * (KD + 1) * sizeof(i64);
+}
+
+template <int KD>
+static int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *pre,
+                       int64_t batch, int64_t Ns, int inverse, int scale, int canon,
+                       cudaStream_t st)
+{
+    int G;
+    int threads = pass_threads(KD, p->M, &G);
+    size_t smem = pass_smem<KD>(G);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_pass<KD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pass_smem<KD>(256 / KD));
+        attr_set = true;
+    }
+    PassArgs A;
+    A.in = in;
+    A.out = out;
+    A.table = scale ? p->table_ninv : p->table;
+    A.pre = pre;
+    A.N = p->N;
+    A.M = p->M;
+    A.Ns = Ns;
+    A.batch_stride = (int64_t)KD * p->N;
+    A.neg_exp = inverse;
+    A.rot_inv = inverse ^ p->root_inv;
+    A.root_inv = p->root_inv;
+    A.scale = scale;
+    A.canon = canon;
+    A.rc = p->rc;
+    dim3 grid((unsigned)((p->M + G - 1) / G), (unsigned)batch);
+    k_pass<KD><<<grid, threads, smem, st>>>(A);
+    return cuda_status();
+}
+
+static int run_transform(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, const u64 *pre,
+                         int64_t batch, int inverse, cudaStream_t st)
+{
+    // ping-pong so that the last pass lands in `out`; `in` is never written
+    int e = p->e;
+    const u64 *src = in;
+    int64_t Ns = 1;
+    for (int pass = 0; pass < e; pass++) {
+        int remaining = e - pass;  // passes left including this one
+        u64 *dst = (remaining % 2 == 1) ? out : work;
+        if (dst == src)
+            dst = (dst == out) ? work : out;
+        int last = pass == e - 1;
+        int scale = inverse && last;
+        const u64 *pre_p = pass == 0 ? pre : nullptr;
+        int rcode;
+        DISPATCH_FAST_K(p->k, (rcode = launch_pass<KD>(p, src, dst, pre_p, batch, Ns, inverse,
+                                                       scale, last, st)));
+        if (rcode)
+            return rcode;
+        p->last_launches++;
+        src = dst;
+        Ns *= p->K;
+    }
+    if (src != out) {
+        cudaMemcpyAsync(out, src, sizeof(u64) * (size_t)p->k * p->N * batch,
+                        cudaMemcpyDeviceToDevice, st);
+    }
+    return cuda_status();
+}
+
+extern "C" {
+
+int gfp_fft_plan_create(gfp_fft_plan **plan, int k, uint64_t r, int K, int e,
+                        const uint64_t *omega, void *stream)
+{
+    if (!plan)
+        return GFP_EINVAL;
+    *plan = nullptr;
+    int err = check_kr(k, r);
+    if (err)
+        return err;
+    if (K != 8 && K != 16 && K != 32 && K != 64)
+        return GFP_EINVAL;
+    if (e < 1)
+        return GFP_EINVAL;
+    if (K != 2 * k)
+        return GFP_EINVAL;
+    int64_t N = 1;
+    for (int i = 0; i < e; i++) {
+        N *= K;
+        if (N > ((int64_t)1 << 40))
+            return GFP_EINVAL;
+    }
+    for (int d = 0; d < k; d++)
+        if (omega[d] > r)
+            return GFP_EINVAL;
+    RadixConsts rc = make_consts(k, r);
+    if (rc.stages_per_norm <= 0)
+        return GFP_EUNSUPPORTED;
+    cudaStream_t st = (cudaStream_t)stream;
+    gfp_fft_plan *p = (gfp_fft_plan *)calloc(1, sizeof(gfp_fft_plan));
+    if (!p)
+        return GFP_ENOMEM;
+    p->k = k;
+    p->K = K;
+    p->e = e;
+    p->N = N;
+    p->M = N / K;
+    p->r = r;
+    p->rc = rc;
+
+    // ---- validate omega like build_plan (fft.py:250-267): omega^N = 1,
+    // omega^(N/2) = -1, omega^(N/2k) in {r, r^(2k-1)}
+    u64 *d_buf = nullptr;
+    size_t words = (size_t)k * 8;
+    if (cudaMalloc(&d_buf, sizeof(u64) * words) != cudaSuccess) {
+        free(p);
+        return GFP_ENOMEM;
+    }
+    // d_buf: [0] omega (digit-major == element-major for n=1), [1..3] results
+    cudaMemcpyAsync(d_buf, omega, sizeof(u64) * k, cudaMemcpyHostToDevice, st);
+    u64 exps[3] = {(u64)N, (u64)(N / 2), (u64)(N / (2 * k))};
+    for (int i = 0; i < 3; i++) {
+        err = gfp_vec_pow(d_buf, &exps[i], 1, d_buf + (size_t)(i + 1) * k, 1, k, r, stream);
+        if (err)
+            break;
+    }
+    u64 h_res[3 * 128];
+    if (!err && cudaMemcpyAsync(h_res, d_buf + k, sizeof(u64) * 3 * k, cudaMemcpyDeviceToHost,
+                                st) != cudaSuccess)
+        err = GFP_ECUDA;
+    if (!err && cudaStreamSynchronize(st) != cudaSuccess)
+        err = GFP_ECUDA;
+    if (!err) {
+        bool one = true, mone = true, fwd = true, inv = true;
+        for (int d = 0; d < k; d++) {
+            if (h_res[d] != (u64)(d == 0))
+                one = false;
+            if (h_res[k + d] != (d == k - 1 ? r : 0))
+                mone = false;
+            // r as an element: digit 1 = 1 (k >= 2)
+            if (h_res[2 * k + d] != (u64)(d == 1))
+                fwd = false;
+        }
+        // 1/r = r^(2k-1) = -(r^(k-1)) = p - r^(k-1) = (r - 1) r^(k-1) + 1
+        for (int d = 0; d < k; d++) {
+            u64 want = (d == k - 1 ? r - 1 : 0) + (d == 0 ? 1 : 0);
+            if (h_res[2 * k + d] != want)
+                inv = false;
+        }
+        if (!one || !mone || !(fwd || inv))
+            err = GFP_EINVAL;
+        p->root_inv = fwd ? 0 : 1;
+    }
+    if (err) {
+        cudaFree(d_buf);
+        free(p);
+        return err;
+    }
+
+    // ---- twiddle tables: omega^b (b < M) and omega^b * N^-1
+    int nsq = 0;
+    while (((int64_t)1 << nsq) < p->M)
+        nsq++;
+    u64 *d_sq = nullptr;
+    size_t tbytes = sizeof(u64) * (size_t)k * p->M;
+    if (cudaMalloc(&p->table, tbytes) != cudaSuccess ||
+        cudaMalloc(&p->table_ninv, tbytes) != cudaSuccess ||
+        cudaMalloc(&d_sq, sizeof(u64) * (size_t)k * (nsq + 1)) != cudaSuccess) {
+        cudaFree(p->table);
+        cudaFree(p->table_ninv);
+        cudaFree(d_sq);
+        cudaFree(d_buf);
+        free(p);
+        return GFP_ENOMEM;
+    }
+    // N^-1 = -(r^k / N) mod p (N | r^k = p - 1): radix-r long division of
+    // r^k by N on the host, then negation with the canonical subtract
+    u64 q[128], ninv[128], zero[128];
+    {
+        u128 rem = 1;  // digit k of r^k
+        for (int i = k - 1; i >= 0; i--) {
+            u128 cur = rem * r;
+            q[i] = (u64)(cur / (u64)N);
+            rem = cur % (u64)N;
+        }
+        for (int d = 0; d < k; d++)
+            zero[d] = 0;
+        dev_gfp_sub(zero, q, ninv, k, r);
+    }
+    cudaMemcpyAsync(d_buf, ninv, sizeof(u64) * k, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_buf + k, omega, sizeof(u64) * k, cudaMemcpyHostToDevice, st);
+    DISPATCH_FAST_K(k, (k_squarings<KD><<<1, 32, 0, st>>>(d_buf + k, d_sq, nsq, rc)));
+    DISPATCH_FAST_K(k, (k_power_table<KD><<<grid_for(p->M, 64), 64, 0, st>>>(d_sq, nsq, p->table,
+                                                                           p->M, rc)));
+    DISPATCH_FAST_K(k, (k_table_scale<KD><<<grid_for(p->M, 64), 64, 0, st>>>(
+                           p->table, d_buf, p->table_ninv, p->M, rc)));
+    err = cuda_status();
+    if (!err && cudaStreamSynchronize(st) != cudaSuccess)
+        err = GFP_ECUDA;
+    cudaFree(d_sq);
+    cudaFree(d_buf);
+    if (err) {
+        cudaFree(p->table);
+        cudaFree(p->table_ninv);
+        free(p);
+        return err;
+    }
+    *plan = p;
+    return GFP_OK;
+}
+
+int gfp_fft_plan_destroy(gfp_fft_plan *p)
+{
+    if (!p)
+        return GFP_OK;
+    cudaFree(p->table);
+    cudaFree(p->table_ninv);
+    cudaFree(p->h_dev);
+    free(p);
+    return GFP_OK;
+}
+
+int64_t gfp_fft_plan_size(const gfp_fft_plan *p) { return p ? p->N : 0; }
+
+int64_t gfp_fft_workspace_words(const gfp_fft_plan *p, int64_t batch)
+{
+    return p ? 2 * (int64_t)p->k * p->N * batch : 0;
+}
+
+int64_t gfp_fft_plan_last_launches(const gfp_fft_plan *p) { return p ? p->last_launches : 0; }
+
+int gfp_fft_exec(const gfp_fft_plan *cp, const uint64_t *in, uint64_t *out, uint64_t *work,
+                 int64_t batch, int inverse, void *stream)
+{
+    gfp_fft_plan *p = const_cast<gfp_fft_plan *>(cp);
+    if (!p || !in || !out || !work || batch < 1)
+        return GFP_EINVAL;
+    p->last_launches = 0;
+    return run_transform(p, in, out, work, nullptr, batch, inverse ? 1 : 0,
+                         (cudaStream_t)stream);
+}
+
+int gfp_poly_mul(const gfp_fft_plan *cp, const uint64_t *f, const uint64_t *g, uint64_t *out,
+                 uint64_t *work, int64_t batch, void *stream)
+{
+    gfp_fft_plan *p = const_cast<gfp_fft_plan *>(cp);
+    if (!p || !f || !g || !out || !work || batch < 1)
+        return GFP_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    p->last_launches = 0;
+    int64_t vw = (int64_t)p->k * p->N * batch;
+    u64 *G = work;        // DFT(g)
+    u64 *scratch = work + vw;
+    int err = run_transform(p, f, out, scratch, nullptr, batch, 0, st);  // out = DFT(f)
+    if (!err)
+        err = run_transform(p, g, G, scratch, nullptr, batch, 0, st);    // G = DFT(g)
+    if (!err)  // out = IDFT(out .* G), the pointwise product fused into pass 0
+        err = run_transform(p, out, out, scratch, G, batch, 1, st);
+    return err;
+}
+
+static int ensure_host_scratch(gfp_fft_plan *p, int64_t words)
+{
+    if (p->h_words >= words)
+        return GFP_OK;
+    cudaFree(p->h_dev);
+    p->h_dev = nullptr;
+    p->h_words = 0;
+    if (cudaMalloc(&p->h_dev, sizeof(u64) * (size_t)words) != cudaSuccess)
+        return GFP_ENOMEM;
+    p->h_words = words;
+    return GFP_OK;
+}
+
+int gfp_fft_exec_host(gfp_fft_plan *p, uint64_t *v, int64_t batch, int inverse, void *stream)
+{
+    if (!p || !v || batch < 1)
+        return GFP_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t vw = (int64_t)p->k * p->N * batch;
+    int err = ensure_host_scratch(p, 3 * vw);
+    if (err)
+        return err;
+    u64 *a = p->h_dev, *b = a + vw, *w = b + vw;
+    cudaMemcpyAsync(a, v, sizeof(u64) * vw, cudaMemcpyHostToDevice, st);
+    p->last_launches = 0;
+    for (int64_t i = 0; i < batch; i++)
+        gfp_to_digit_major(a + i * p->k * p->N, b + i * p->k * p->N, p->N, p->k, st);
+    err = run_transform(p, b, b, w, nullptr, batch, inverse ? 1 : 0, st);
+    if (err)
+        return err;
+    for (int64_t i = 0; i < batch; i++)
+        gfp_to_element_major(b + i * p->k * p->N, a + i * p->k * p->N, p->N, p->k, st);
+    p->last_launches += 2 * batch;
+    cudaMemcpyAsync(v, a, sizeof(u64) * vw, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess)
+        return GFP_ECUDA;
+    return cuda_status();
+}
+
+int gfp_poly_mul_host(gfp_fft_plan *p, const uint64_t *f, const uint64_t *g, uint64_t *out,
+                      int64_t batch, void *stream)
+{
+    if (!p || !f || !g || !out || batch < 1)
+        return GFP_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t vw = (int64_t)p->k * p->N * batch;
+    int err = ensure_host_scratch(p, 6 * vw);
+    if (err)
+        return err;
+    u64 *hf = p->h_dev, *hg = hf + vw, *df = hg + vw, *dg = df + vw, *w = dg + vw;
+    cudaMemcpyAsync(hf, f, sizeof(u64) * vw, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(hg, g, sizeof(u64) * vw, cudaMemcpyHostToDevice, st);
+    for (int64_t i = 0; i < batch; i++) {
+        gfp_to_digit_major(hf + i * p->k * p->N, df + i * p->k * p->N, p->N, p->k, st);
+        gfp_to_digit_major(hg + i * p->k * p->N, dg + i * p->k * p->N, p->N, p->k, st);
+    }
+    err = gfp_poly_mul(p, df, dg, df, w, batch, st);
+    if (err)
+        return err;
+    for (int64_t i = 0; i < batch; i++)
+        gfp_to_element_major(df + i * p->k * p->N, hf + i * p->k * p->N, p->N, p->k, st);
+    p->last_launches += 3 * batch;
+    cudaMemcpyAsync(out, hf, sizeof(u64) * vw, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess)
+        return GFP_ECUDA;
+    return cuda_status();
+}
+
+}  // extern "C"
