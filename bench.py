@@ -1,0 +1,555 @@
+#!/usr/bin/env python
+"""Benchmark of the GF(r^k+1) FFT / poly-multiply path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c1|c3|c4|c5] [--no-extra]
+
+Default workload: BASELINE.json configs[1] (C2), the polynomial product of
+two degree-(2^15 - 1) polynomials over p = r^8 + 1 (r = 2^59 + 2^16) through
+2^16-point transforms.  A step is one poly-multiply (two forward DFTs, the
+pointwise product fused into the inverse's first pass, the inverse with the
+N^-1 scale fused into its last pass).  Inputs are resident in HBM; the 4 MiB
+operands fit in L2, so a 256 MiB buffer is written between timed steps (L2
+flush) and every step is timed with its own CUDA events on the launching
+stream.  value = output coefficients per second (N per poly-multiply, all
+ranks); ms_per_step = poly-multiply time.
+
+Multi-GPU (torchrun): C2 does not shard -- every rank runs an independent
+replica ("replicas only", weak scaling); C3 splits its batch of transforms
+across ranks with no collective.
+
+--impl reference: the reference's CPU algorithm (oracle/gfp_oracle.c, a C
+restatement of gfpfft's dft_general / gfp_mul_fft -- the reference itself is
+pure Python and does not travel to the GPU box), on all host threads, same
+workload and metric; rank 0 only.
+"""
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "Z/pZ FFT elements/s (k=8,16; N=2^12..2^24), poly-mul time, % roofline"
+R = {8: (1 << 59) + (1 << 16), 16: (1 << 58) + (1 << 10), 32: (1 << 56) + (1 << 21)}
+
+# workload table: (k, K, e, batch, kind, seeds)
+WORKLOADS = {
+    "c1": dict(k=8, K=16, e=3, batch=1, kind="fwd+inv", name="C1 fwd+inv k=8 N=2^12"),
+    "c2": dict(k=8, K=16, e=4, batch=1, kind="polymul",
+               name="C2 poly-mul k=8 N=2^16 (deg 2^15-1 x deg 2^15-1)"),
+    "c3": dict(k=16, K=32, e=4, batch=64, kind="fwd", name="C3 batched fwd k=16 64 x N=2^20"),
+    "c4": dict(k=8, K=16, e=6, batch=1, kind="fwd", name="C4 fwd k=8 N=2^24"),
+    "c5": dict(k=32, K=64, e=3, batch=1, kind="mul+fwd",
+               name="C5 2^22 muls + fwd N=2^18, k=32"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work model (counts what the kernels are asked to compute)
+
+def mults_per_transform(N, K, inverse=False, pre=False):
+    """General Z/pZ multiplies one transform performs: per Stockham pass,
+    element (j, t) is multiplied when its twiddle omega^E has a non-unit
+    omega^b part (E mod N/K != 0), every element on the inverse's last pass
+    (N^-1 folded in), and every element of pass 0 when a pointwise operand
+    is fused in."""
+    M = N // K
+    e = 0
+    n = N
+    while n > 1:
+        n //= K
+        e += 1
+    total = 0
+    Ns = 1
+    for p in range(e):
+        last = p == e - 1
+        if inverse and last:
+            total += N
+        elif Ns > 1:
+            # count (j, t), j < M, t < K with t * (j mod Ns) * (M / Ns) != 0 mod M
+            # <=> t * (j mod Ns) != 0 mod Ns; for fixed t exactly gcd(t, Ns)
+            # residues j mod Ns give 0
+            from math import gcd
+            per_block = sum(Ns - gcd(t, Ns) for t in range(K))
+            total += per_block * (M // Ns)
+        if pre and p == 0:
+            total += N
+        Ns *= K
+    return total
+
+
+def passes(N, K):
+    e = 0
+    while N > 1:
+        N //= K
+        e += 1
+    return e
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# distributed helpers
+
+def dist_setup():
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, ws):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm (oracle = C restatement of the reference)
+
+def cpu_poly_mul_rate(budget_s, threads):
+    from oracle import oracle as O
+    k, K, e = 8, 16, 4
+    N = K ** e
+    r = R[k]
+    _, w = O.gfp_root(k, r, N)
+    plan = O.Plan(k, r, K, e, w)
+    plan.prepare_inverse()
+    f = __import__("numpy").zeros((N, k), dtype="uint64")
+    g = f.copy()
+    f[: N // 2] = O.random_elements(1, k, r, N // 2)
+    g[: N // 2] = O.random_elements(2, k, r, N // 2)
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while True:
+        t0 = time.perf_counter()
+        plan.poly_mul(f, g, threads=threads)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end:
+            break
+    per = statistics.median(times)
+    return N / per, per, len(times)
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    threads = O.lib().orc_max_threads() if hasattr(O.lib(), "orc_max_threads") else 1
+    threads = max(1, os.cpu_count() or 1)
+    wl = WORKLOADS["c2"]
+    k, K, e = wl["k"], wl["K"], wl["e"]
+    N = K ** e
+    r = R[k]
+    _, w = O.gfp_root(k, r, N)
+    plan = O.Plan(k, r, K, e, w)
+    plan.prepare_inverse()
+    import numpy as np
+    f = np.zeros((N, k), dtype=np.uint64)
+    g = f.copy()
+    f[: N // 2] = O.random_elements(1, k, r, N // 2)
+    g[: N // 2] = O.random_elements(2, k, r, N // 2)
+    for _ in range(args.warmup):
+        plan.poly_mul(f, g, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = plan.poly_mul(f, g, threads=threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    assert O.digest(out) == "ad746dbbdda033dd", "reference arm lost parity"
+    value = N / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "elements/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (reference seeds 1, 2)",
+        "config": {"workload": wl["name"], "k": k, "r": r, "K": K, "e": e, "N": N,
+                   "parallelism": "cpu-omp%d" % threads},
+        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": threads,
+                         "kind": "port",
+                         "sample": "full C2 poly-mul per step (oracle/gfp_oracle.c, "
+                                   "gfp_mul_fft restated, OpenMP over base-case blocks)"},
+        "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def probe_int_peak():
+    from paper_1811_01490_b200 import _lib
+    import torch
+    lib = _lib.load()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    best = 0.0
+    for _ in range(3):
+        ms = ctypes.c_float()
+        ops = ctypes.c_double()
+        _lib.check(lib.gfp_probe_imad_wide(4000, sms * 8, 256, ctypes.byref(ms),
+                                           ctypes.byref(ops),
+                                           ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        best = max(best, ops.value / (ms.value * 1e-3))
+    return best
+
+
+def setup_c2():
+    import numpy as np
+    import torch
+    import paper_1811_01490_b200 as gp
+    wl = WORKLOADS["c2"]
+    k, K, e = wl["k"], wl["K"], wl["e"]
+    N = K ** e
+    params = gp.GfpParams(R[k], k)
+    field = gp.GfpFftField(params, backend="cuda")
+    omega = gp.roots_for(params, N)
+    plan = gp.build_plan(field, K, e, omega)
+    # synthetic inputs with the reference's distribution: the low half of
+    # each operand uniform residues, the high half zero (degree 2^15 - 1)
+    f = torch.zeros((k, N), dtype=torch.int64, device="cuda").view(torch.uint64)
+    g = torch.zeros((k, N), dtype=torch.int64, device="cuda").view(torch.uint64)
+    half = gp.vec.uniform(N // 2, params, seed=1)
+    f.view(torch.int64)[:, : N // 2] = half.view(torch.int64)
+    half = gp.vec.uniform(N // 2, params, seed=2)
+    g.view(torch.int64)[:, : N // 2] = half.view(torch.int64)
+    return gp, params, plan, f, g, N, k, K
+
+
+def timed_loop(step, steps, warmup, ws, flush, stream):
+    import torch
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(ws)
+    evs = []
+    for _ in range(steps):
+        flush()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    barrier(ws)
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def run_ours(args, ws, rank, local):
+    import numpy as np
+    import torch
+    import paper_1811_01490_b200 as gp
+    from paper_1811_01490_b200 import _lib
+    dev = torch.device("cuda", local if ws > 1 else 0)
+    stream = torch.cuda.current_stream()
+    flush_buf = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > L2
+
+    def flush():
+        flush_buf.zero_()
+
+    gp_, params, plan, f, g, N, k, K = setup_c2()
+    out = torch.empty_like(f)
+    work = torch.empty(int(_lib.load().gfp_fft_workspace_words(plan.handle, 1)),
+                       dtype=torch.uint64, device=dev)
+    lib = _lib.load()
+    sp = ctypes.c_void_p
+
+    def direct():
+        _lib.check(lib.gfp_poly_mul(plan.handle, sp(f.data_ptr()), sp(g.data_ptr()),
+                                    sp(out.data_ptr()), sp(work.data_ptr()), 1,
+                                    sp(torch.cuda.current_stream().cuda_stream)))
+
+    # parity guard on the timed configuration: the reference's own inputs
+    # (Random(1), Random(2)) must reproduce the reference's product digest
+    from_ref = None
+    try:
+        from oracle import oracle as O
+        fo = np.zeros((N, k), dtype=np.uint64)
+        go = fo.copy()
+        fo[: N // 2] = O.random_elements(1, k, R[k], N // 2)
+        go[: N // 2] = O.random_elements(2, k, R[k], N // 2)
+        prod = gp.vec.to_host(gp.poly_mul(gp.vec.to_device(fo, k), gp.vec.to_device(go, k),
+                                          plan))
+        from_ref = O.digest(prod) == "ad746dbbdda033dd"
+        if not from_ref:
+            raise SystemExit("C2 parity check failed before timing")
+    except ImportError:
+        pass
+
+    # capture the poly-multiply in a CUDA graph (12 pass kernels)
+    direct()
+    launches_per_step = int(lib.gfp_fft_plan_last_launches(plan.handle))
+    graph = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        direct()
+        with torch.cuda.graph(graph, stream=s):
+            direct()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+
+    def step():
+        graph.replay()
+
+    sampler = ClockSampler(local if ws > 1 else 0)
+    sampler.start()
+    times = timed_loop(step, args.steps, args.warmup, ws, flush, stream)
+    clocks = sampler.stop()
+    ms = sum(times) / len(times)
+    ms_max = max_over_ranks(ms, ws)
+    value = ws * N / (ms_max * 1e-3)
+
+    # ---- roofline of the dominant kernel (k_pass<8>: every launch of the step)
+    mults = (2 * mults_per_transform(N, K) + mults_per_transform(N, K, inverse=True, pre=True))
+    imad = mults * 4 * k * k
+    peak_imad = probe_int_peak()
+    achieved = imad / (ms * 1e-3)
+    npass = 3 * passes(N, K)
+    hbm_bytes = npass * 2 * k * N * 8 + N * k * 8  # vector reads + writes, + pointwise operand
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = prof.get("c2_step_dram_bytes")
+    except (OSError, ValueError):
+        pass
+
+    # ---- e2e: host buffers through the C-ABI host entry point
+    pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
+    fh = pin(gp.vec.to_host(f))
+    gh = pin(gp.vec.to_host(g))
+    oh = torch.empty_like(fh).pin_memory()
+
+    def e2e_step():
+        _lib.check(lib.gfp_poly_mul_host(plan.handle, sp(fh.data_ptr()), sp(gh.data_ptr()),
+                                         sp(oh.data_ptr()), 1,
+                                         sp(torch.cuda.current_stream().cuda_stream)))
+
+    e2e_times = timed_loop(e2e_step, max(3, args.steps // 2), args.warmup, ws, flush, stream)
+    e2e_ms = max_over_ranks(sum(e2e_times) / len(e2e_times), ws)
+    e2e_launches = int(lib.gfp_fft_plan_last_launches(plan.handle))
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (device-seeded uniform residues, reference shapes); parity "
+                "guard with the reference's Random(1)/Random(2) inputs passed"
+                if from_ref else "synthetic (device-seeded uniform residues)",
+        "config": {"workload": WORKLOADS["c2"]["name"], "k": k, "r": R[k], "K": K, "e": 4,
+                   "N": N, "batch_per_gpu": 1, "parallelism": "replicas x%d" % ws,
+                   "l2": "256 MiB buffer written between timed steps (inputs fit in L2)",
+                   "graph": "CUDA graph of the 12 pass kernels per step"},
+        "roofline": {"bound": "int", "kernel": "k_pass<8> (all launches of the step)",
+                     "achieved": achieved / 1e12, "peak": peak_imad / 1e12,
+                     "unit": "T IMAD.WIDE/s", "frac": achieved / peak_imad,
+                     "traffic": traffic,
+                     "algorithmic": "%d general multiplies x 4k^2 = %d IMAD.WIDE per step"
+                                    % (mults, imad),
+                     "peak_source": "measured live: gfp_probe_imad_wide (8 independent "
+                                    "mad.wide.s32 chains/thread, best of 3)"},
+        "roofline_hbm": {"bound": "hbm", "achieved": hbm_bytes / (ms * 1e-3) / 1e9,
+                         "peak": hbm_peak, "unit": "GB/s",
+                         "frac": hbm_bytes / (ms * 1e-3) / 1e9 / hbm_peak,
+                         "algorithmic_bytes_per_step": hbm_bytes,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+        "e2e": {"value": ws * N / (e2e_ms * 1e-3), "unit": "elements/s",
+                "ms_per_step": e2e_ms, "h2d_bytes_per_step": 2 * N * k * 8,
+                "d2h_bytes_per_step": N * k * 8,
+                "api": "gfp_poly_mul_host (C-ABI, pinned host buffers, element-major)"},
+        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches_per_step": launches_per_step,
+        "e2e_gpu_launches_per_step": e2e_launches,
+        "clocks": clocks,
+    }
+    if rank == 0 and not args.no_cpu:
+        try:
+            threads = os.cpu_count() or 1
+            v, per, n = cpu_poly_mul_rate(args.cpu_budget, threads)
+            line["cpu_baseline"] = {
+                "value": v, "unit": "elements/s", "cores": threads, "kind": "port",
+                "sample": "%d full C2 poly-muls (%.3f s each), oracle/gfp_oracle.c "
+                          "(gfp_mul_fft + dft_general restated), OpenMP" % (n, per)}
+        except Exception as exc:  # the oracle is optional on exotic hosts
+            line["cpu_baseline"] = {"value": None, "error": str(exc)[:200]}
+    if rank == 0 and not args.no_extra:
+        line["configs"] = extra_configs(args, dev, flush, stream)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def extra_configs(args, dev, flush, stream):
+    """The other BASELINE.json configs, timed briefly (elements/s)."""
+    import torch
+    import paper_1811_01490_b200 as gp
+    res = {}
+    steps = max(3, min(args.steps, 10))
+    for key in ("c1", "c4", "c3", "c5"):
+        wl = WORKLOADS[key]
+        try:
+            k, K, e, B = wl["k"], wl["K"], wl["e"], wl["batch"]
+            N = K ** e
+            params = gp.GfpParams(R[k], k)
+            field = gp.GfpFftField(params, backend="cuda")
+            plan = gp.build_plan(field, K, e, gp.roots_for(params, N))
+            x = gp.vec.uniform(N, params, seed=7, batch=B if B > 1 else None)
+            y = torch.empty_like(x)
+            entry = {"workload": wl["name"]}
+            if key == "c1":
+                def step():
+                    gp.fft_tensor(x, plan, out=y)
+                    gp.fft_tensor(y, plan, inverse=True, out=y)
+                t = timed_loop(step, steps, 2, 1, flush, stream)
+                ms = sum(t) / len(t)
+                entry.update(ms_fwd_plus_inv=ms, elements_per_s=N / (ms * 1e-3))
+            elif key in ("c3", "c4"):
+                def step():
+                    gp.fft_tensor(x, plan, out=y)
+                t = timed_loop(step, steps, 2, 1, flush, stream)
+                ms = sum(t) / len(t)
+                mults = B * mults_per_transform(N, K)
+                entry.update(ms_fwd=ms, elements_per_s=B * N / (ms * 1e-3),
+                             tera_imad_per_s=mults * 4 * k * k / (ms * 1e-3) / 1e12)
+            else:
+                n = 1 << 22
+                a = gp.vec.uniform(n, params, seed=51)
+                b = gp.vec.uniform(n, params, seed=52)
+
+                def mstep():
+                    gp.vec.mul(a, b, params)
+                t = timed_loop(mstep, steps, 2, 1, flush, stream)
+                ms = sum(t) / len(t)
+                entry.update(ms_mul=ms, muls_per_s=n / (ms * 1e-3),
+                             tera_imad_per_s=n * 4 * k * k / (ms * 1e-3) / 1e12)
+
+                def step():
+                    gp.fft_tensor(x, plan, out=y)
+                t = timed_loop(step, steps, 2, 1, flush, stream)
+                ms = sum(t) / len(t)
+                entry.update(ms_fwd=ms, fft_elements_per_s=N / (ms * 1e-3))
+            res[key] = entry
+            del x, y
+            torch.cuda.empty_cache()
+        except Exception as exc:
+            res[key] = {"error": str(exc)[:300]}
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c2"])
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -34,10 +34,11 @@ struct RadixConsts {
     u64 bias_lo;    // 2^63 * r as a 128-bit constant (fast-multiply bias)
     u64 bias_hi;
     double rinv;    // 1.0 / r (quotient estimates for small quotients)
+    u64 m_recip;    // floor(2^(64+w) / r) - 2^64 (fast-multiply quotient estimate)
     int sh;         // leading zeros of r
-    int s;          // limb split for the fast multiply: digit = hi * 2^s + lo
+    int w;          // bit length of r (64 - sh)
+    int s;          // limb split of the fast multiply (digit = hi 2^s + lo), 0 = no fast path
     int stages_per_norm;  // lazy radix-2 stages allowed between normalisations
-    int pad;
 };
 
 // ---------------------------------------------------------------------------

@@ -42,58 +42,53 @@ static int ilog2_exact(int64_t v)
 
 static bool valid_k(int k) { return k >= 1 && k <= 128 && (k & (k - 1)) == 0; }
 
-// Fast-path (limb split) bound check; exact integer arithmetic.  Returns
-// true and fills s / stages when every accumulation bound of fast_mul_lazy
-// and the lazy butterflies holds for digits in [-delta, r + delta].
+static int fast_split_for(int k) { return k <= 8 ? 30 : 29; }  // FastSplit<KD>::S
+
+// Fast-path bound check, exact integer arithmetic.  Returns true and fills
+// s / stages when every accumulation bound of fast_mul_lazy (gfp_fast.cuh)
+// and of the lazy butterflies holds for digits in [-delta, r + delta].
 static bool fast_bounds(int k, u64 r, int *s_out, int *stages_out)
 {
     if (!(k == 4 || k == 8 || k == 16 || k == 32))
         return false;
-    if (r < ((u64)1 << 24) || r >= ((u64)1 << 62))
+    if (r < ((u64)1 << 24) || r >= ((u64)1 << 62) || (r & (r - 1)) == 0)
         return false;
     const u128 two63 = (u128)1 << 63;
     int K = 2 * k;
     int logK = ilog2_exact(K);
-    // stages between normalisations: 2^S (r + delta) < 2^62 with delta = 2^S + k + 8
+    // stages between normalisations: 2^S (r + delta) < 2^63 with delta = 2^S + k + 8
     int S = 0;
     for (int t = 1; t <= logK; t++) {
         u128 delta = ((u128)1 << t) + (u64)k + 8;
-        if ((((u128)r + delta) << t) < ((u128)1 << 62))
+        if ((((u128)r + delta) << t) < two63)
             S = t;
     }
     if (S < 1)
         return false;
     u128 delta = ((u128)1 << S) + (u64)k + 8;
-    u128 X = (u128)r + delta;  // |lazy digit| bound
-    u128 Y = X;
-    for (int s = 31; s >= 20; s--) {
-        u128 L = ((u128)1 << s) - 1;
-        u128 Xh = (X >> s) + 1;
-        u128 Yh = (Y >> s) + 1;
-        if (Xh >= ((u128)1 << 31) || Yh >= ((u128)1 << 31))
-            continue;
-        u128 kk = (u128)k;
-        if (kk * L * L >= two63 || kk * L * Yh >= two63 || kk * Xh * L >= two63 ||
-            kk * Xh * Yh >= two63)
-            continue;
-        // |c| <= k X Y must satisfy k X Y < 2^63 r (bias keeps c + 2^63 r in [0, 2^64 r))
-        // compare k X Y / r < 2^63 without overflow: X, Y < 2^62 so X*Y < 2^124
-        u128 XY = X * Y;
-        u128 qmax = (XY / r) * kk + kk;  // |q| bound after the first division
-        if (qmax >= two63)
-            continue;
-        // second round input |e| <= r + qmax < 2^63
-        if ((u128)r + qmax + 2 >= two63)
-            continue;
-        // output delta' = (r + qmax) / r + 2 must be <= delta
-        u128 d2 = ((u128)r + qmax) / r + 2;
-        if (d2 > delta)
-            continue;
-        *s_out = s;
-        *stages_out = S;
-        return true;
-    }
-    return false;
+    u128 X = (u128)r + delta;  // |lazy digit| bound (both operands)
+    int s = fast_split_for(k);
+    u128 L = ((u128)1 << s) - 1;
+    u128 Xh = (X >> s) + 1;
+    u128 kk = (u128)k;
+    if (Xh >= ((u128)1 << 31))
+        return false;
+    // the four sub-column sums stay below 2^63 in magnitude
+    if (kk * L * L >= two63 || kk * L * Xh >= two63 || kk * Xh * Xh >= two63)
+        return false;
+    // |c| <= k X^2 < 2^63 r keeps c + 2^63 r in [0, 2^64 r)
+    u128 qmax = (X * X / r) * kk + kk;  // >= |c| / r
+    if (qmax >= two63 - 8)
+        return false;
+    // second carry round: |rem + q| <= 4r + qmax < 2^63
+    if (4 * (u128)r + qmax + 2 >= two63)
+        return false;
+    // its quotient lands within delta: (4r + qmax) / r + 2 <= delta
+    if ((4 * (u128)r + qmax) / r + 2 > delta)
+        return false;
+    *s_out = s;
+    *stages_out = S;
+    return true;
 }
 
 static RadixConsts make_consts(int k, u64 r)
@@ -110,6 +105,11 @@ static RadixConsts make_consts(int k, u64 r)
     c.bias_lo = (u64)bias;
     c.bias_hi = (u64)(bias >> 64);
     c.rinv = 1.0 / (double)r;
+    c.w = 64 - c.sh;
+    if (c.w < 64) {
+        u128 m = ((u128)1 << (64 + c.w)) / r;
+        c.m_recip = (u64)(m - ((u128)1 << 64));
+    }
     int s = 0, S = 0;
     if (fast_bounds(k, r, &s, &S)) {
         c.s = s;

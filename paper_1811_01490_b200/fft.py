@@ -97,7 +97,8 @@ class FftPlan:
             while (1 << bit) < M:
                 mask = ((j >> bit) & 1).bool()
                 prod = vec.mul(out, sq, self.params)
-                out = torch.where(mask.unsqueeze(0), prod, out)
+                out = torch.where(mask.unsqueeze(0), prod.view(torch.int64),
+                                  out.view(torch.int64)).view(torch.uint64).contiguous()
                 sq = vec.mul(sq, sq, self.params)
                 bit += 1
             self._table = vec.to_tuples(out)
@@ -317,12 +318,14 @@ def twiddle_apply(v, m, n, omega_i, field, offset=0):
     rows = [vec.to_device([field.one()], k)]
     for _ in range(1, n):
         rows.append(vec.mul(rows[-1], w, params))
-    row = torch.cat(rows, dim=1)                                  # [k, n]
-    factors = [torch.cat([vec.to_device([field.one()], k)] * n, dim=1)]
+    i64 = torch.int64
+    row = torch.cat([t.view(i64) for t in rows], dim=1).contiguous().view(torch.uint64)
+    ones = vec.to_device([field.one()] * n, k)
+    factors = [ones]
     for _ in range(1, m):
         factors.append(vec.mul(factors[-1], row, params))
-    F = torch.stack(factors, dim=2).reshape(k, n * m)             # index j*m + i
-    res = vec.mul(block, F.contiguous(), params)
+    F = torch.stack([t.view(i64) for t in factors], dim=2).reshape(k, n * m)  # j*m + i
+    res = vec.mul(block, F.contiguous().view(torch.uint64), params)
     v[offset:offset + m * n] = vec.to_tuples(res)
     return v
 

@@ -1,0 +1,71 @@
+"""Host-side logic of the package (no GPU): parameter validation, encode /
+decode, canonical checks, list utilities, compat reports."""
+import random
+
+import pytest
+
+import paper_1811_01490_b200 as gp
+
+R8 = (1 << 59) + (1 << 16)
+
+
+def test_params_validation():
+    # tests/test_gfp_field.py:38-50
+    with pytest.raises(ValueError):
+        gp.GfpParams(10, 3)
+    with pytest.raises(ValueError):
+        gp.GfpParams(10, 0)
+    with pytest.raises(ValueError):
+        gp.GfpParams(1, 8)
+    with pytest.raises(ValueError):
+        gp.GfpParams(1 << 64, 8)
+    assert gp.GfpParams(10, 4).p == 10 ** 4 + 1
+
+
+@pytest.mark.parametrize("k,r", [(8, R8), (16, (1 << 58) + (1 << 10)), (1, 4), (2, 6),
+                                 (4, 10), (8, 2)])
+def test_encode_decode_bijection(k, r):
+    params = gp.GfpParams(r, k)
+    rng = random.Random(7)
+    vals = [0, 1, r - 1, r, params.p - 2, params.p - 1] + \
+        [rng.randrange(params.p) for _ in range(200)]
+    for v in vals:
+        v %= params.p
+        x = gp.gfp_encode(params, v)
+        assert gp.is_canonical(params, x)
+        assert gp.gfp_decode(params, x) == v
+    assert gp.gfp_encode(params, params.p - 1) == (0,) * (k - 1) + (r,)
+
+
+def test_canonical_rejects():
+    params = gp.GfpParams(10, 4)
+    assert not gp.is_canonical(params, (10, 0, 0, 0))
+    assert not gp.is_canonical(params, (1, 0, 0, 10))
+    assert not gp.is_canonical(params, (0, 0, 0))
+    with pytest.raises(ValueError):
+        gp.gfp_decode(params, (0, 11, 0, 0))
+
+
+def test_text_roundtrip():
+    params = gp.GfpParams(R8, 8)
+    x = gp.gfp_encode(params, 123456789 ** 5)
+    assert gp.element_from_text(params, gp.element_to_text(x)) == x
+    with pytest.raises(ValueError):
+        gp.element_from_text(params, "1,2")
+
+
+def test_stride_permutation_example():
+    # tests/test_fft.py:56-58
+    assert gp.stride_permutation(list(range(8)), 2, 4) == [0, 2, 4, 6, 1, 3, 5, 7]
+    v = list(range(24))
+    gp.stride_permutation(v, 3, 4)
+    gp.stride_permutation(v, 4, 3)
+    assert v == list(range(24))
+
+
+def test_compat_report():
+    params = gp.GfpParams((1 << 63) + (1 << 34), 8)
+    rep = gp.check_prime_compat(params, gp.crt_default())
+    assert not rep.passed and rep.slack < 0
+    ok = gp.check_prime_compat(gp.GfpParams(R8, 8), gp.crt_default())
+    assert ok.passed and ok.slack > 0
