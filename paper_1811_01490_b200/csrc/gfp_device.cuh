@@ -35,10 +35,18 @@ struct RadixConsts {
     u64 bias_hi;
     double rinv;    // 1.0 / r (quotient estimates for small quotients)
     u64 m_recip;    // floor(2^(64+w) / r) - 2^64 (fast-multiply quotient estimate)
+    u64 bias_t;     // (2^63 r) >> w
+    i64 sp_mask;    // 2^sp_a - 1
+    i64 sp_half;    // 2^(sp_a - 1)
     int sh;         // leading zeros of r
     int w;          // bit length of r (64 - sh)
     int s;          // limb split of the fast multiply (digit = hi 2^s + lo), 0 = no fast path
     int stages_per_norm;  // lazy radix-2 stages allowed between normalisations
+    int sp_on;      // sparse radix r = 2^sp_a + sp_eps: shift-based normalisation
+    int sp_a;
+    int sp_eps;
+    int q_sh1;      // max(w - 2S, 0) and max(2S - w, 0) for column_quot
+    int q_sh2;
 };
 
 // ---------------------------------------------------------------------------
@@ -92,6 +100,63 @@ GFP_D i64 floordiv_small(i64 v, const RadixConsts &rc, i64 &rem)
     }
     rem = rr;
     return q;
+}
+
+// 32x32 -> 64 signed multiply-add in one IMAD.WIDE (the compiler otherwise
+// may widen to a 64x64 multiply)
+GFP_D i64 mad_wide_s32(int a, int b, i64 c)
+{
+    i64 d;
+    asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+    return d;
+}
+
+// Balanced lazy normaliser: v = q r + rem with q small and
+// rem in [-r/2 - ex, r/2 + ex] (the host bound check fixes ex).  For the
+// paper's sparse radices r = 2^a + eps it is a shift, a mask and one
+// IMAD.WIDE:
+//   q = (v + 2^(a-1)) >> a,  rem = ((v + 2^(a-1)) mod 2^a) - 2^(a-1) - q eps;
+// otherwise a rounded division through a double estimate (one fix-up).
+template <bool SPARSE>
+GFP_D int norm_bal(i64 v, const RadixConsts &rc, i64 &rem)
+{
+    if (SPARSE) {
+        const i64 vb = v + rc.sp_half;
+        const int q = (int)(vb >> rc.sp_a);
+        rem = mad_wide_s32(-q, rc.sp_eps, (vb & rc.sp_mask) - rc.sp_half);
+        return q;
+    }
+    const double est = (double)v * rc.rinv;
+    i64 q = __double2ll_rn(est);
+    i64 rr = v - q * (i64)rc.r;
+    const i64 h = (i64)(rc.r >> 1);
+    if (rr > h) {
+        q += 1;
+        rr -= (i64)rc.r;
+    } else if (rr < -h) {
+        q -= 1;
+        rr += (i64)rc.r;
+    }
+    rem = rr;
+    return (int)q;
+}
+
+// Canonical digits [0, r] to balanced lazy digits: a digit above r/2 becomes
+// d - r with a carry of +1 into the next digit (negated into digit 0, since
+// r^k = -1).  The value is unchanged mod p.
+template <int KD>
+GFP_D void to_balanced(i64 (&x)[KD], u64 r)
+{
+    const i64 h = (i64)(r >> 1);
+    int c[KD];
+#pragma unroll
+    for (int i = 0; i < KD; i++) {
+        c[i] = x[i] > h;
+        x[i] -= c[i] ? (i64)r : 0;
+    }
+#pragma unroll
+    for (int i = 0; i < KD; i++)
+        x[i] += i ? c[i - 1] : -c[KD - 1];
 }
 
 // ---------------------------------------------------------------------------
@@ -209,28 +274,26 @@ GFP_HD void finish_canonical(DZ &z, int k, u64 r, int C)
     }
 }
 
-// Lazy digits (signed, |f_i - r/2| well below 2^62, |carry| small relative
-// to r) to canonical.  Exact; loops until the wrap carry is in {-1, 0, 1}.
+// Lazy digits in [-delta, r + delta] (delta < r / 4, host-verified) to the
+// canonical encoding.  One carry pass keeps every carry in {-1, 0, 1}; the
+// wrap carry C (value = D + C r^k = D - C mod p) is then resolved by
+// finish_canonical, including the form-B cases.
 template <typename DF, typename DZ>
 GFP_D void lazy_to_canonical(const DF &f, DZ &z, int k, const RadixConsts &rc)
 {
-    i64 C = 0;
+    const i64 r = (i64)rc.r;
+    int C = 0;
     for (int i = 0; i < k; i++) {
-        i64 rem;
-        i64 q = floordiv_small((i64)f[i] + C, rc, rem);
-        z[i] = (u64)rem;
-        C = q;
-    }
-    // value = D + C r^k = D - C (mod p)
-    while (C > 1 || C < -1) {
-        i64 carry = -C;
-        for (int i = 0; i < k; i++) {
-            i64 rem;
-            i64 q = floordiv_small((i64)z[i] + carry, rc, rem);
-            z[i] = (u64)rem;
-            carry = q;
+        i64 t = (i64)f[i] + C;
+        C = 0;
+        if (t < 0) {
+            t += r;
+            C = -1;
+        } else if (t >= r) {
+            t -= r;
+            C = 1;
         }
-        C = carry;
+        z[i] = (u64)t;
     }
-    finish_canonical(z, k, rc.r, (int)C);
+    finish_canonical(z, k, rc.r, C);
 }

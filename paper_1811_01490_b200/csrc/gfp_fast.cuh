@@ -3,98 +3,119 @@
 // fast_mul_lazy: x * y mod p for lazy signed digits, the Z/pZ twiddle,
 // pointwise and N^-1 multiply of the transform (the role gfp_mul_fft plays
 // for the reference, gfp_mult.py:416-501, paper Alg. 13).  Instead of two
-// word-prime NTTs + CRT + LHC, each digit is split as hi * 2^s + lo (|hi|,
-// lo < 2^31) and the negacyclic convolution is four sub-column sums of
-// 32x32 -> 64 signed IMAD.WIDE products:
+// word-prime NTTs + CRT + LHC, each digit is split as hi * 2^s + lo
+// (balanced limbs, |lo| <= 2^(s-1)) and the negacyclic convolution is three
+// sub-column sums of 32x32 -> 64 signed IMAD.WIDE products:
 //
-//   c_m = LL_m + (LH_m + HL_m) 2^s + HH_m 2^(2s),
-//   XY_m = sum_{i+j=m} x_i y_j - sum_{i+j=m+k} x_i y_j   (r^k = -1).
+//   c_m = LL_m + MID_m 2^s + HH_m 2^(2s),   MID = sum (x_lo y_hi + x_hi y_lo),
+//   XY_m = sum_{i+j=m} x_i y_j - sum_{i+j=m+k} x_i y_j      (r^k = -1),
 //
-// The host verifies (plan time, exact integers) that every sub-column stays
-// below 2^63 in magnitude for the digit bounds the transform guarantees, so
-// the accumulation needs no carries.  Each 128-bit column (biased by 2^63 r
-// to be non-negative) gets a quotient estimate from its top 64 bits times a
-// fixed-point reciprocal of r (at most 3 short, exact remainder from the low
-// word), and two cheap carry rounds leave lazy digits in [-delta, r + delta]
-// with delta <= 2^S + k + 8.
+// with MID from a limb-level Karatsuba product (3 IMAD.WIDE per digit pair).
+//
+// The host verifies (plan time, exact integers: gfp_kernels.cu fast_bounds)
+// that every sub-column stays below 2^63 in magnitude for the digit bounds
+// the transform guarantees, so the accumulation needs no carries.  The
+// quotient of each biased column c' = c + 2^63 r (non-negative, < 2^64 r) by
+// r is estimated from floor(c' / 2^w), which is built from the three 64-bit
+// sub-columns with shifts only (no 128-bit arithmetic), times a fixed-point
+// reciprocal of r; the estimate is at most 3 short, so the remainder is
+// exact from the low 64 bits and lies in [0, 4r).  Two cheap carry rounds
+// (the balanced normaliser, norm_bal) leave balanced lazy digits in
+// [-r/2 - delta, r/2 + delta].
 #pragma once
 #include "gfp_device.cuh"
-
-// 32x32 -> 64 signed multiply-add in one IMAD.WIDE (the compiler otherwise
-// widens to a 64x64 multiply)
-GFP_D i64 mad_wide_s32(int a, int b, i64 c)
-{
-    i64 d;
-    asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
-    return d;
-}
 
 // limb split used by the fast multiply for each k (compile time; the host
 // bound check in gfp_kernels.cu:fast_bounds verifies it for the given r)
 template <int KD>
 struct FastSplit {
-    static constexpr int S = KD <= 8 ? 30 : 29;
+    static constexpr int S = KD <= 16 ? 29 : 28;
 };
 
-// floor(c' / r) for 0 <= c' < 2^64 r, up to 3 short: q in [q* - 3, q*], and
-// the exact remainder c' - q r in [0, 4r) from the low word alone.
-GFP_D u64 quot_est(u64 hi, u64 lo, const RadixConsts &rc, u64 &rem)
+// quotient estimate and exact remainder of the biased column
+//   c' = HH 2^(2S) + MID 2^S + LL + 2^63 r,  0 <= c' < 2^64 r
+template <int S>
+GFP_D u64 column_quot(i64 LL, i64 MID, i64 HH, const RadixConsts &rc, u64 &rem)
 {
-    const int w = rc.w;  // bit length of r
-    u64 t = (hi << (64 - w)) | (lo >> w);
-    u64 q = t + __umul64hi(t, rc.m_recip);
-    rem = lo - q * rc.r;
+    // floor(c / 2^w) from nested floors of shifts (no 128-bit arithmetic):
+    //   w >= 2S:  (HH + (mid >> S)) >> (w - 2S)
+    //   w <  2S:  (HH << (2S - w)) + (mid >> (w - S))
+    // folded into one branch-free form with sh1 = max(w - 2S, 0),
+    // sh2 = max(2S - w, 0) (host-computed)
+    const i64 mid = MID + (LL >> S);  // floor((MID 2^S + LL) / 2^S)
+    const i64 t0 = ((HH << rc.q_sh2) + (mid >> (S - rc.q_sh2))) >> rc.q_sh1;
+    const u64 t = (u64)t0 + rc.bias_t;  // floor(c' / 2^w), in [0, 2^64)
+    const u64 clo = (u64)LL + ((u64)MID << S) + ((u64)HH << (2 * S)) + rc.bias_lo;
+    const u64 q = t + __umul64hi(t, rc.m_recip);
+    rem = clo - q * rc.r;
     return q;
 }
 
-template <int KD>
+// x * y mod p for balanced lazy digits (|digit| <= r/2 + delta), output
+// balanced lazy digits.  Limbs are balanced too, x = xh 2^S + xl with
+// xl in [-2^(S-1), 2^(S-1)), and the middle sub-column comes from one
+// Karatsuba product per digit pair:
+//   MID = sum (xl + xh)(yl + yh) - LL - HH,
+// so a digit product costs three IMAD.WIDE instead of four.
+template <int KD, bool SPARSE>
 GFP_D void fast_mul_lazy(const i64 (&x)[KD], const i64 (&y)[KD], i64 (&f)[KD],
                          const RadixConsts &rc)
 {
     constexpr int S = FastSplit<KD>::S;
-    constexpr i64 mask = ((i64)1 << S) - 1;
-    int xl[KD], xh[KD], yl[KD], yh[KD], nyl[KD], nyh[KD];
+    constexpr i64 half = (i64)1 << (S - 1);
+    int xl[KD], xh[KD], xs[KD], yl[KD], yh[KD], ys[KD];
 #pragma unroll
     for (int i = 0; i < KD; i++) {
-        xl[i] = (int)(x[i] & mask);
-        xh[i] = (int)(x[i] >> S);
-        yl[i] = (int)(y[i] & mask);
-        yh[i] = (int)(y[i] >> S);
-        nyl[i] = -yl[i];
-        nyh[i] = -yh[i];
+        xh[i] = (int)((x[i] + half) >> S);
+        xl[i] = (int)(x[i] - ((i64)xh[i] << S));
+        xs[i] = xl[i] + xh[i];
+        yh[i] = (int)((y[i] + half) >> S);
+        yl[i] = (int)(y[i] - ((i64)yh[i] << S));
+        ys[i] = yl[i] + yh[i];
     }
-    const u128 bias = ((u128)rc.bias_hi << 64) | rc.bias_lo;
-    i64 q[KD];
-    u64 d[KD];
+    // Columns in order, with the two carry rounds streaming behind them:
+    //   round 1  c_m = q_m r + d_m                       (column_quot)
+    //   round 2  d_m + q_{m-1} = q2_m r + d2_m            (norm_bal)
+    //   round 3  f_m = d2_m + q2_{m-1}
+    // with the r^k = -1 wrap at m = 0 (q_{-1} = -q_{k-1}).  Only column 0's
+    // remainder and digit 1's pending carry wait for the last column.
+    i64 q_prev = 0, d0 = 0, f1 = 0;
+    int q2_prev = 0;
 #pragma unroll
     for (int m = 0; m < KD; m++) {
-        i64 LL = 0, LH = 0, HL = 0, HH = 0;
+        i64 LL = 0, SS = 0, HH = 0, LLn = 0, SSn = 0, HHn = 0;
 #pragma unroll
-        for (int i = 0; i < KD; i++) {
-            const int j = (m - i + KD) % KD;
-            const bool neg = i > m;
-            const int a = neg ? nyl[j] : yl[j];
-            const int b = neg ? nyh[j] : yh[j];
-            LL = mad_wide_s32(xl[i], a, LL);
-            LH = mad_wide_s32(xl[i], b, LH);
-            HL = mad_wide_s32(xh[i], a, HL);
-            HH = mad_wide_s32(xh[i], b, HH);
+        for (int i = 0; i <= m; i++) {
+            LL = mad_wide_s32(xl[i], yl[m - i], LL);
+            SS = mad_wide_s32(xs[i], ys[m - i], SS);
+            HH = mad_wide_s32(xh[i], yh[m - i], HH);
         }
-        // c' = c + 2^63 r, exact and non-negative (host-verified bounds)
-        u128 c = bias + (u128)(i128)LL + (u128)((i128)LH << S) + (u128)((i128)HL << S) +
-                 (u128)((i128)HH << (2 * S));
+#pragma unroll
+        for (int i = m + 1; i < KD; i++) {  // wrapped terms: r^k = -1
+            LLn = mad_wide_s32(xl[i], yl[m - i + KD], LLn);
+            SSn = mad_wide_s32(xs[i], ys[m - i + KD], SSn);
+            HHn = mad_wide_s32(xh[i], yh[m - i + KD], HHn);
+        }
+        LL -= LLn;
+        HH -= HHn;
+        const i64 MID = (SS - SSn) - LL - HH;
         u64 rem;
-        u64 qq = quot_est((u64)(c >> 64), (u64)c, rc, rem);
-        q[m] = (i64)(qq - (1ULL << 63));
-        d[m] = rem;  // in [0, 4r)
+        const u64 qq = column_quot<S>(LL, MID, HH, rc, rem);
+        if (m == 0) {
+            d0 = (i64)rem;
+        } else {
+            i64 d2;
+            const int q2 = norm_bal<SPARSE>((i64)rem + q_prev, rc, d2);
+            if (m == 1)
+                f1 = d2;  // + q2_0, known only after the last column
+            else
+                f[m] = d2 + q2_prev;
+            q2_prev = q2;
+        }
+        q_prev = (i64)(qq - (1ULL << 63));
     }
-    i64 q2[KD], d2[KD];
-#pragma unroll
-    for (int m = 0; m < KD; m++) {
-        i64 cin = m ? q[m - 1] : -q[KD - 1];
-        q2[m] = floordiv_small((i64)d[m] + cin, rc, d2[m]);
-    }
-#pragma unroll
-    for (int m = 0; m < KD; m++)
-        f[m] = d2[m] + (m ? q2[m - 1] : -q2[KD - 1]);
+    i64 d2_0;
+    const int q2_0 = norm_bal<SPARSE>(d0 - q_prev, rc, d2_0);
+    f[0] = d2_0 - q2_prev;
+    f[1] = f1 + q2_0;
 }

@@ -42,52 +42,111 @@ static int ilog2_exact(int64_t v)
 
 static bool valid_k(int k) { return k >= 1 && k <= 128 && (k & (k - 1)) == 0; }
 
-static int fast_split_for(int k) { return k <= 8 ? 30 : 29; }  // FastSplit<KD>::S
+static int fast_split_for(int k) { return k <= 16 ? 29 : 28; }  // FastSplit<KD>::S
+
+struct FastPlan {
+    int S;        // lazy radix-2 stages between normalisations
+    int sp_on;    // sparse-radix normalisation (r = 2^a + eps, |eps| small)
+    int sp_a;
+    i64 sp_eps;
+    u128 delta;   // balanced lazy digits stay in [-r/2 - delta, r/2 + delta]
+};
+
+// balanced normaliser (norm_bal) on |v| <= V: the quotient bound and the
+// excess it leaves over [-r/2, r/2]
+static void norm_bounds(u128 V, u64 r, const FastPlan &fp, u128 *qmax, u128 *ex)
+{
+    if (fp.sp_on) {
+        u128 q = ((V + ((u128)1 << (fp.sp_a - 1))) >> fp.sp_a) + 1;
+        u128 e = (u128)(fp.sp_eps < 0 ? -fp.sp_eps : fp.sp_eps);
+        *qmax = q;
+        *ex = q * (e + 1) + e / 2 + 2;
+    } else {
+        u128 q = V / r + 2;
+        *qmax = q;
+        *ex = q + 2;
+    }
+}
 
 // Fast-path bound check, exact integer arithmetic.  Returns true and fills
-// s / stages when every accumulation bound of fast_mul_lazy (gfp_fast.cuh)
-// and of the lazy butterflies holds for digits in [-delta, r + delta].
-static bool fast_bounds(int k, u64 r, int *s_out, int *stages_out)
+// `fp` when every bound of fast_mul_lazy (gfp_fast.cuh) and of the lazy
+// butterflies (k_pass) holds for balanced digits |d| <= X = r/2 + delta:
+//   * 2^S X + 2^a < 2^63 (S unnormalised radix-2 stages, then norm_bal);
+//   * the sub-column sums LL, SS, HH (and MID = SS - LL - HH,
+//     MID + (LL >> s)) of the balanced-limb product stay below 2^63;
+//   * k X^2 < 2^63 r (the biased column c + 2^63 r is in [0, 2^64 r));
+//   * the carry rounds stay within 2^63 and land back inside delta.
+static bool fast_bounds(int k, u64 r, FastPlan *out)
 {
     if (!(k == 4 || k == 8 || k == 16 || k == 32))
         return false;
     if (r < ((u64)1 << 24) || r >= ((u64)1 << 62) || (r & (r - 1)) == 0)
         return false;
     const u128 two63 = (u128)1 << 63;
-    int K = 2 * k;
-    int logK = ilog2_exact(K);
-    // stages between normalisations: 2^S (r + delta) < 2^63 with delta = 2^S + k + 8
-    int S = 0;
-    for (int t = 1; t <= logK; t++) {
-        u128 delta = ((u128)1 << t) + (u64)k + 8;
-        if ((((u128)r + delta) << t) < two63)
-            S = t;
+    const int K = 2 * k;
+    const int logK = ilog2_exact(K);
+    const u128 kk = (u128)k;
+    FastPlan fp;
+    memset(&fp, 0, sizeof(fp));
+    // sparse radix: r = 2^a + eps with 2^a the nearest power of two
+    int w = 64 - __builtin_clzll(r);
+    u64 lo_p = (u64)1 << (w - 1);
+    u64 hi_p = (u64)1 << w;
+    if (r - lo_p <= hi_p - r) {
+        fp.sp_a = w - 1;
+        fp.sp_eps = (i64)(r - lo_p);
+    } else {
+        fp.sp_a = w;
+        fp.sp_eps = -(i64)(hi_p - r);
     }
-    if (S < 1)
+    i64 aeps = fp.sp_eps < 0 ? -fp.sp_eps : fp.sp_eps;
+    fp.sp_on = aeps < ((i64)1 << 30) && fp.sp_a >= 40 && (aeps << 20) < ((i64)1 << fp.sp_a);
+    const int s = fast_split_for(k);
+    const u128 half = (u128)1 << (s - 1);
+    const u128 top = (u128)1 << (fp.sp_on ? fp.sp_a : w);
+    u128 delta = 2;  // canonical inputs enter through to_balanced (excess <= 1)
+    for (int iter = 0; iter < 16; iter++) {
+        u128 X = (u128)(r / 2) + delta;
+        int S = 0;
+        for (int t = 1; t <= logK; t++)
+            if ((X << t) + top < two63)
+                S = t;
+        if (S < 1)
+            return false;
+        fp.S = S;
+        u128 q1, ex1;
+        norm_bounds(X << S, r, fp, &q1, &ex1);
+        // multiply: balanced limbs, |xl| <= 2^(s-1), |xh| <= H, |xs| <= 2^(s-1) + H
+        u128 H = (X + half) >> s;
+        u128 Hs = half + H;
+        if (Hs >= ((u128)1 << 31))
+            return false;
+        if (kk * half * half >= two63 || kk * H * H >= two63 || kk * Hs * Hs >= two63)
+            return false;
+        if (2 * kk * half * H + kk * half * half / ((u128)1 << s) + 2 >= two63)
+            return false;
+        if (w < 2 * s && ((kk * H * H) << (2 * s - w)) >= two63)
+            return false;
+        u128 XX = X * X;
+        if (XX / r * kk + kk + 8 >= two63)
+            return false;
+        u128 Q1 = XX / r * kk + kk + 8;  // |column quotient|
+        u128 E = 4 * (u128)r + Q1;       // |rem + carry| after round 1
+        if (E + top >= two63)
+            return false;
+        u128 q2, ex2;
+        norm_bounds(E, r, fp, &q2, &ex2);
+        u128 need = ex1 > ex2 ? ex1 : ex2;
+        if (need <= delta)
+            break;
+        delta = need;
+        if (iter == 15)
+            return false;
+    }
+    if (delta * 8 >= r)
         return false;
-    u128 delta = ((u128)1 << S) + (u64)k + 8;
-    u128 X = (u128)r + delta;  // |lazy digit| bound (both operands)
-    int s = fast_split_for(k);
-    u128 L = ((u128)1 << s) - 1;
-    u128 Xh = (X >> s) + 1;
-    u128 kk = (u128)k;
-    if (Xh >= ((u128)1 << 31))
-        return false;
-    // the four sub-column sums stay below 2^63 in magnitude
-    if (kk * L * L >= two63 || kk * L * Xh >= two63 || kk * Xh * Xh >= two63)
-        return false;
-    // |c| <= k X^2 < 2^63 r keeps c + 2^63 r in [0, 2^64 r)
-    u128 qmax = (X * X / r) * kk + kk;  // >= |c| / r
-    if (qmax >= two63 - 8)
-        return false;
-    // second carry round: |rem + q| <= 4r + qmax < 2^63
-    if (4 * (u128)r + qmax + 2 >= two63)
-        return false;
-    // its quotient lands within delta: (4r + qmax) / r + 2 <= delta
-    if ((4 * (u128)r + qmax) / r + 2 > delta)
-        return false;
-    *s_out = s;
-    *stages_out = S;
+    fp.delta = delta;
+    *out = fp;
     return true;
 }
 
@@ -110,10 +169,18 @@ static RadixConsts make_consts(int k, u64 r)
         u128 m = ((u128)1 << (64 + c.w)) / r;
         c.m_recip = (u64)(m - ((u128)1 << 64));
     }
-    int s = 0, S = 0;
-    if (fast_bounds(k, r, &s, &S)) {
-        c.s = s;
-        c.stages_per_norm = S;
+    FastPlan fp;
+    if (fast_bounds(k, r, &fp)) {
+        c.s = fast_split_for(k);
+        c.stages_per_norm = fp.S;
+        c.sp_on = fp.sp_on;
+        c.sp_a = fp.sp_a;
+        c.sp_eps = (int)fp.sp_eps;
+        c.sp_mask = ((i64)1 << fp.sp_a) - 1;
+        c.sp_half = (i64)1 << (fp.sp_a - 1);
+        c.q_sh1 = c.w > 2 * c.s ? c.w - 2 * c.s : 0;
+        c.q_sh2 = c.w < 2 * c.s ? 2 * c.s - c.w : 0;
+        c.bias_t = r << (63 - c.w);
     } else {
         c.s = 0;
         c.stages_per_norm = 0;
@@ -213,7 +280,7 @@ __global__ void k_mul_generic(const u64 *__restrict__ x, const u64 *__restrict__
     }
 }
 
-template <int KD>
+template <int KD, bool SPARSE>
 __global__ void k_mul_fast(const u64 *__restrict__ x, const u64 *__restrict__ y, int64_t y_inc,
                            u64 *__restrict__ z, int64_t n, RadixConsts rc)
 {
@@ -228,7 +295,9 @@ __global__ void k_mul_fast(const u64 *__restrict__ x, const u64 *__restrict__ y,
             a[d] = (i64)x[d * n + i];
             b[d] = (i64)y[d * yn + iy];
         }
-        fast_mul_lazy<KD>(a, b, f, rc);
+        to_balanced<KD>(a, rc.r);
+        to_balanced<KD>(b, rc.r);
+        fast_mul_lazy<KD, SPARSE>(a, b, f, rc);
         lazy_to_canonical(f, c, KD, rc);
 #pragma unroll
         for (int d = 0; d < KD; d++)
@@ -313,13 +382,15 @@ struct PassArgs {
     u64 *out;
     const u64 *table;  // element-major [M][k] canonical, omega^b (or omega^b / N)
     const u64 *pre;    // optional pointwise operand, digit-major like `in`
-    int64_t N, M, Ns;
     int64_t batch_stride;
+    int lN, lM, lNs;   // log2 of N, M = N/K and Ns (all powers of two)
+    int lG;            // log2 of the groups per CTA
     int neg_exp;   // twiddle exponent N - E (inverse transform)
     int rot_inv;   // base-case root of this execution is 1/r (rotations by r^-t)
     int root_inv;  // the plan's omega^M is 1/r (twiddle split r^-a omega^b)
     int scale;     // every element gets a table multiply (N^-1 folded in)
     int canon;     // canonical output (last pass)
+    int in_canon;  // input digits are canonical (convert to balanced on load)
     RadixConsts rc;
 };
 
@@ -334,14 +405,15 @@ GFP_D i64 rot_lane(i64 val, int t, int d, bool inverse)
     return neg ? -v : v;
 }
 
-template <int KD>
+// one lazy normalisation of a digit held one-digit-per-lane: the quotient
+// moves one lane up (negated into digit 0: r^k = -1)
+template <int KD, bool SPARSE>
 GFP_D void normalize_lane(i64 &v, int d, const RadixConsts &rc)
 {
     i64 rem;
-    i64 q = floordiv_small(v, rc, rem);
-    int qi = (int)q;
-    int qin = __shfl_sync(FULL_MASK, qi, (d - 1) & (KD - 1), KD);
-    v = rem + (d == 0 ? -(i64)qin : (i64)qin);
+    int q = norm_bal<SPARSE>(v, rc, rem);
+    int qin = __shfl_sync(FULL_MASK, q, (d - 1) & (KD - 1), KD);
+    v = rem + (d == 0 ? -qin : qin);
 }
 
 template <int K>
@@ -355,17 +427,26 @@ __host__ __device__ constexpr int bitrev_c(int x)
     return y;
 }
 
-template <int KD>
+// One radix-K Stockham pass over `batch` vectors (grid.y), G = 2^lG groups
+// of K elements per CTA.  Group j reads x[j + t M] (t < K), multiplies by
+// omega^E, E = t (j mod Ns) (M / Ns), and writes the K-point DFT to
+// (j / Ns) Ns K + (j mod Ns) + u Ns.  After log_K N passes the output is the
+// natural-order DFT (the reference's dft_general result, fft.py:298-360).
+template <int KD, bool SPARSE>
 __global__ void __launch_bounds__(256) k_pass(PassArgs A)
 {
     constexpr int K = 2 * KD;
+    constexpr int LK = KD == 4 ? 3 : KD == 8 ? 4 : KD == 16 ? 5 : 6;
     constexpr int ROW = KD + 1;  // padded smem row (bank spread)
     extern __shared__ i64 sm[];  // [K][G][ROW]
-    const int G = blockDim.x / KD;
+    const int lG = A.lG;
+    const int G = 1 << lG;
     const int tid = threadIdx.x;
     const int64_t bidx = blockIdx.y;
-    const int64_t j0 = (int64_t)blockIdx.x * G;
-    const int64_t N = A.N, M = A.M, Ns = A.Ns;
+    const int64_t j0 = (int64_t)blockIdx.x << lG;
+    const int lN = A.lN, lM = A.lM, lNs = A.lNs;
+    const int64_t N = (int64_t)1 << lN, M = (int64_t)1 << lM;
+    const int64_t nsmask = ((int64_t)1 << lNs) - 1;
     const u64 *in = A.in + bidx * A.batch_stride;
     u64 *out = A.out + bidx * A.batch_stride;
     const u64 *pre = A.pre ? A.pre + bidx * A.batch_stride : nullptr;
@@ -374,30 +455,31 @@ __global__ void __launch_bounds__(256) k_pass(PassArgs A)
     // ---- phase A: load K elements per group, twiddle / pointwise multiply
 #pragma unroll 1
     for (int h = 0; h < 2; h++) {
-        const int g = tid % G;
-        const int t = tid / G + h * KD;
+        const int g = tid & (G - 1);
+        const int t = (tid >> lG) + h * KD;
         const int64_t j = j0 + g;
         i64 x[KD];
         int a = 0;
         if (j < M) {
-            const int64_t pos = j + (int64_t)t * M;
+            const int64_t pos = j + ((int64_t)t << lM);
 #pragma unroll
             for (int d = 0; d < KD; d++)
-                x[d] = (i64)__ldg(in + d * N + pos);
+                x[d] = (i64)__ldg(in + ((int64_t)d << lN) + pos);
+            if (A.in_canon)
+                to_balanced<KD>(x, rc.r);
             if (pre) {
                 i64 y[KD];
 #pragma unroll
                 for (int d = 0; d < KD; d++)
-                    y[d] = (i64)__ldg(pre + d * N + pos);
-                fast_mul_lazy<KD>(x, y, x, rc);
+                    y[d] = (i64)__ldg(pre + ((int64_t)d << lN) + pos);
+                fast_mul_lazy<KD, SPARSE>(x, y, x, rc);
             }
-            int64_t E = 0;
-            if (Ns > 1)
-                E = (int64_t)t * (j % Ns) * (M / Ns);
+            // E = t (j mod Ns) (M / Ns) < N; omega^E = (omega^M)^a omega^b
+            int64_t E = ((int64_t)t * (j & nsmask)) << (lM - lNs);
             if (A.neg_exp && E)
                 E = N - E;
-            a = (int)(E / M);
-            const int64_t b = E - (int64_t)a * M;
+            a = (int)(E >> lM);
+            const int64_t b = E & (M - 1);
             // omega^M is r (or 1/r for plans built on an inverse root)
             if (A.root_inv && a)
                 a = 2 * KD - a;
@@ -410,7 +492,7 @@ __global__ void __launch_bounds__(256) k_pass(PassArgs A)
                     y[d] = (i64)w.x;
                     y[d + 1] = (i64)w.y;
                 }
-                fast_mul_lazy<KD>(x, y, x, rc);
+                fast_mul_lazy<KD, SPARSE>(x, y, x, rc);
             }
         } else {
 #pragma unroll
@@ -418,7 +500,7 @@ __global__ void __launch_bounds__(256) k_pass(PassArgs A)
                 x[d] = 0;
         }
         // x * r^a: rotation by a (0 <= a < 2k), wrapped digits negated
-        i64 *row = sm + ((int64_t)t * G + g) * ROW;
+        i64 *row = sm + (((int64_t)t << lG) + g) * ROW;
 #pragma unroll
         for (int d = 0; d < KD; d++) {
             int p = d + a;
@@ -438,13 +520,13 @@ __global__ void __launch_bounds__(256) k_pass(PassArgs A)
 
     // ---- phase B: K-point DFT at root r (or 1/r), one digit per lane
     {
-        const int d = tid % KD;
+        const int d = tid & (KD - 1);
         const int g = tid / KD;
         const bool inv = A.rot_inv != 0;
         i64 v[K];
 #pragma unroll
         for (int t = 0; t < K; t++)
-            v[t] = sm[((int64_t)t * G + g) * ROW + d];
+            v[t] = sm[(((int64_t)t << lG) + g) * ROW + d];
         const int S = rc.stages_per_norm;
         int stage = 0;
 #pragma unroll
@@ -464,29 +546,29 @@ __global__ void __launch_bounds__(256) k_pass(PassArgs A)
             if (len > 1 && stage % S == 0) {
 #pragma unroll
                 for (int t = 0; t < K; t++)
-                    normalize_lane<KD>(v[t], d, rc);
+                    normalize_lane<KD, SPARSE>(v[t], d, rc);
             }
         }
 #pragma unroll
         for (int t = 0; t < K; t++)
-            normalize_lane<KD>(v[t], d, rc);
+            normalize_lane<KD, SPARSE>(v[t], d, rc);
         __syncthreads();
 #pragma unroll
         for (int t = 0; t < K; t++)
-            sm[((int64_t)bitrev_c<K>(t) * G + g) * ROW + d] = v[t];
+            sm[(((int64_t)bitrev_c<K>(t) << lG) + g) * ROW + d] = v[t];
     }
     __syncthreads();
 
     // ---- phase C: store in Stockham order (canonicalise on the last pass)
 #pragma unroll 1
     for (int h = 0; h < 2; h++) {
-        const int g = tid % G;
-        const int u = tid / G + h * KD;
+        const int g = tid & (G - 1);
+        const int u = (tid >> lG) + h * KD;
         const int64_t j = j0 + g;
         if (j >= M)
             continue;
-        const int64_t pos = (j / Ns) * Ns * K + (j % Ns) + (int64_t)u * Ns;
-        const i64 *row = sm + ((int64_t)u * G + g) * ROW;
+        const int64_t pos = ((j >> lNs) << (lNs + LK)) + (j & nsmask) + ((int64_t)u << lNs);
+        const i64 *row = sm + (((int64_t)u << lG) + g) * ROW;
         if (A.canon) {
             i64 f[KD];
             u64 c[KD];
@@ -496,11 +578,11 @@ __global__ void __launch_bounds__(256) k_pass(PassArgs A)
             lazy_to_canonical(f, c, KD, rc);
 #pragma unroll
             for (int d = 0; d < KD; d++)
-                out[d * N + pos] = c[d];
+                out[((int64_t)d << lN) + pos] = c[d];
         } else {
 #pragma unroll
             for (int d = 0; d < KD; d++)
-                out[d * N + pos] = (u64)row[d];
+                out[((int64_t)d << lN) + pos] = (u64)row[d];
         }
     }
 }
@@ -562,6 +644,24 @@ __global__ void k_table_scale(const u64 *__restrict__ tab, const u64 *__restrict
         gfp_mul_generic<KD>(a, y, z, rc);
         for (int d = 0; d < KD; d++)
             out[b * KD + d] = z[d];
+    }
+}
+
+// element-major canonical table entries -> balanced lazy digits (in place);
+// the transform multiplies balanced operands only
+template <int KD>
+__global__ void k_table_balance(u64 *__restrict__ tab, int64_t n, u64 r)
+{
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        i64 x[KD];
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            x[d] = (i64)tab[b * KD + d];
+        to_balanced<KD>(x, r);
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            tab[b * KD + d] = (u64)x[d];
     }
 }
 
@@ -655,8 +755,8 @@ int gfp_check_prime_compat(int k, uint64_t r)
 
 int gfp_fast_path_ok(int k, uint64_t r)
 {
-    int s, S;
-    return fast_bounds(k, r, &s, &S) ? 1 : 0;
+    FastPlan fp;
+    return fast_bounds(k, r, &fp) ? 1 : 0;
 }
 
 static int check_kr(int k, u64 r)
@@ -712,8 +812,13 @@ int gfp_vec_mul(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z
     cudaStream_t st = (cudaStream_t)stream;
     RadixConsts rc = make_consts(k, r);
     if (rc.stages_per_norm > 0) {
-        DISPATCH_FAST_K(k, (k_mul_fast<KD><<<grid_for(n, 128), 128, 0, st>>>(x, y, y_inc, z, n,
-                                                                             rc)));
+        if (rc.sp_on) {
+            DISPATCH_FAST_K(k, (k_mul_fast<KD, true><<<grid_for(n, 128), 128, 0, st>>>(
+                                   x, y, y_inc, z, n, rc)));
+        } else {
+            DISPATCH_FAST_K(k, (k_mul_fast<KD, false><<<grid_for(n, 128), 128, 0, st>>>(
+                                   x, y, y_inc, z, n, rc)));
+        }
     } else {
         DISPATCH_K(k, (k_mul_generic<KD><<<grid_for(n, 128), 128, 0, st>>>(x, y, y_inc, z, n,
                                                                            rc)));
@@ -832,14 +937,16 @@ static size_t pass_smem(int G)
 template <int KD>
 static int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *pre,
                        int64_t batch, int64_t Ns, int inverse, int scale, int canon,
-                       cudaStream_t st)
+                       int in_canon, cudaStream_t st)
 {
     int G;
     int threads = pass_threads(KD, p->M, &G);
     size_t smem = pass_smem<KD>(G);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_pass<KD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_pass<KD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pass_smem<KD>(256 / KD));
+        cudaFuncSetAttribute(k_pass<KD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)pass_smem<KD>(256 / KD));
         attr_set = true;
     }
@@ -848,23 +955,34 @@ static int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64
     A.out = out;
     A.table = scale ? p->table_ninv : p->table;
     A.pre = pre;
-    A.N = p->N;
-    A.M = p->M;
-    A.Ns = Ns;
     A.batch_stride = (int64_t)KD * p->N;
+    A.lN = ilog2_exact(p->N);
+    A.lM = ilog2_exact(p->M);
+    A.lNs = ilog2_exact(Ns);
+    A.lG = ilog2_exact(G);
     A.neg_exp = inverse;
     A.rot_inv = inverse ^ p->root_inv;
     A.root_inv = p->root_inv;
     A.scale = scale;
     A.canon = canon;
+    A.in_canon = in_canon;
     A.rc = p->rc;
     dim3 grid((unsigned)((p->M + G - 1) / G), (unsigned)batch);
-    k_pass<KD><<<grid, threads, smem, st>>>(A);
+    if (p->rc.sp_on)
+        k_pass<KD, true><<<grid, threads, smem, st>>>(A);
+    else
+        k_pass<KD, false><<<grid, threads, smem, st>>>(A);
     return cuda_status();
 }
 
+// One transform of `batch` vectors.  in_canon: the input is canonical
+// (user data) and is converted to balanced digits on load; out_canon: the
+// last pass canonicalises (user-visible output) -- poly_mul keeps its
+// intermediate spectra as balanced lazy digits.  `pre` is a pointwise
+// operand (balanced lazy) multiplied in on the first pass.
 static int run_transform(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, const u64 *pre,
-                         int64_t batch, int inverse, cudaStream_t st)
+                         int64_t batch, int inverse, int in_canon, int out_canon,
+                         cudaStream_t st)
 {
     // ping-pong so that the last pass lands in `out`; `in` is never written
     int e = p->e;
@@ -880,7 +998,8 @@ static int run_transform(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, co
         const u64 *pre_p = pass == 0 ? pre : nullptr;
         int rcode;
         DISPATCH_FAST_K(p->k, (rcode = launch_pass<KD>(p, src, dst, pre_p, batch, Ns, inverse,
-                                                       scale, last, st)));
+                                                       scale, last && out_canon,
+                                                       pass == 0 && in_canon, st)));
         if (rcode)
             return rcode;
         p->last_launches++;
@@ -1021,6 +1140,9 @@ int gfp_fft_plan_create(gfp_fft_plan **plan, int k, uint64_t r, int K, int e,
                                                                            p->M, rc)));
     DISPATCH_FAST_K(k, (k_table_scale<KD><<<grid_for(p->M, 64), 64, 0, st>>>(
                            p->table, d_buf, p->table_ninv, p->M, rc)));
+    DISPATCH_FAST_K(k, (k_table_balance<KD><<<grid_for(p->M, 128), 128, 0, st>>>(p->table, p->M, r)));
+    DISPATCH_FAST_K(k, (k_table_balance<KD><<<grid_for(p->M, 128), 128, 0, st>>>(p->table_ninv, p->M,
+                                                                                r)));
     err = cuda_status();
     if (!err && cudaStreamSynchronize(st) != cudaSuccess)
         err = GFP_ECUDA;
@@ -1063,7 +1185,7 @@ int gfp_fft_exec(const gfp_fft_plan *cp, const uint64_t *in, uint64_t *out, uint
     if (!p || !in || !out || !work || batch < 1)
         return GFP_EINVAL;
     p->last_launches = 0;
-    return run_transform(p, in, out, work, nullptr, batch, inverse ? 1 : 0,
+    return run_transform(p, in, out, work, nullptr, batch, inverse ? 1 : 0, 1, 1,
                          (cudaStream_t)stream);
 }
 
@@ -1078,11 +1200,12 @@ int gfp_poly_mul(const gfp_fft_plan *cp, const uint64_t *f, const uint64_t *g, u
     int64_t vw = (int64_t)p->k * p->N * batch;
     u64 *G = work;        // DFT(g)
     u64 *scratch = work + vw;
-    int err = run_transform(p, f, out, scratch, nullptr, batch, 0, st);  // out = DFT(f)
+    // spectra stay balanced lazy digits; only the product is canonicalised
+    int err = run_transform(p, f, out, scratch, nullptr, batch, 0, 1, 0, st);  // out = DFT(f)
     if (!err)
-        err = run_transform(p, g, G, scratch, nullptr, batch, 0, st);    // G = DFT(g)
+        err = run_transform(p, g, G, scratch, nullptr, batch, 0, 1, 0, st);    // G = DFT(g)
     if (!err)  // out = IDFT(out .* G), the pointwise product fused into pass 0
-        err = run_transform(p, out, out, scratch, G, batch, 1, st);
+        err = run_transform(p, out, out, scratch, G, batch, 1, 0, 1, st);
     return err;
 }
 
@@ -1113,7 +1236,7 @@ int gfp_fft_exec_host(gfp_fft_plan *p, uint64_t *v, int64_t batch, int inverse, 
     p->last_launches = 0;
     for (int64_t i = 0; i < batch; i++)
         gfp_to_digit_major(a + i * p->k * p->N, b + i * p->k * p->N, p->N, p->k, st);
-    err = run_transform(p, b, b, w, nullptr, batch, inverse ? 1 : 0, st);
+    err = run_transform(p, b, b, w, nullptr, batch, inverse ? 1 : 0, 1, 1, st);
     if (err)
         return err;
     for (int64_t i = 0; i < batch; i++)

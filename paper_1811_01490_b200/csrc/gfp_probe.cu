@@ -12,16 +12,20 @@
 
 __global__ void k_probe_imad_wide(int64_t iters, int a0, int b0, int64_t *out)
 {
-    int a = a0 + threadIdx.x, b = b0 ^ blockIdx.x;
+    int b = b0 ^ blockIdx.x;
     int64_t acc[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; c++)
-        acc[c] = c;
+        acc[c] = c + a0 + threadIdx.x;
     for (int64_t i = 0; i < iters; i++) {
 #pragma unroll
         for (int c = 0; c < NCH; c++) {
+            // the multiplicand depends on the running accumulator, so the
+            // product cannot be hoisted out of the loop
             int64_t d;
-            asm volatile("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a + c), "r"(b), "l"(acc[c]));
+            asm volatile("{\n\t.reg .u32 t;\n\tcvt.u32.u64 t, %1;\n\t"
+                         "mad.wide.s32 %0, t, %2, %1;\n\t}"
+                         : "=l"(d) : "l"(acc[c]), "r"(b + c));
             acc[c] = d;
         }
     }
