@@ -466,10 +466,69 @@ def run_ours(args, ws, rank, local):
                           "(gfp_mul_fft + dft_general restated), OpenMP" % (n, per)}
         except Exception as exc:  # the oracle is optional on exotic hosts
             line["cpu_baseline"] = {"value": None, "error": str(exc)[:200]}
+    multi = {}
+    if not args.no_extra:
+        multi = multi_gpu_configs(args, ws, rank, dev, flush, stream)
     if rank == 0 and not args.no_extra:
         line["configs"] = extra_configs(args, dev, flush, stream)
+        line["configs"].update(multi)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def multi_gpu_configs(args, ws, rank, dev, flush, stream):
+    """The configs that shard, run on every rank:
+    C3 -- 64 independent k=16 transforms split 64/G per GPU, no collective
+          (weak in the sense that per-GPU work shrinks: value = 64 N / time);
+    C4 -- one k=8 2^24-point transform, four-step N1 = N2 = 2^12 with one
+          NCCL all-to-all per direction (strong scaling)."""
+    import torch
+    import paper_1811_01490_b200 as gp
+    from paper_1811_01490_b200.sharded import GpuShardOps, ShardedFFT
+    res = {}
+    steps = max(3, min(args.steps, 10))
+    try:
+        wl = WORKLOADS["c3"]
+        k, K, e = wl["k"], wl["K"], wl["e"]
+        N = K ** e
+        B = 64 // ws
+        params = gp.GfpParams(R[k], k)
+        plan = gp.build_plan(gp.GfpFftField(params, backend="cuda"), K, e,
+                             gp.roots_for(params, N))
+        x = gp.vec.uniform(N, params, seed=300 + rank, batch=B)
+        y = torch.empty_like(x)
+        t = timed_loop(lambda: gp.fft_tensor(x, plan, out=y), steps, 2, ws, flush, stream)
+        ms = max_over_ranks(sum(t) / len(t), ws)
+        res["c3_split"] = {"workload": wl["name"] + " split %d/GPU" % B, "n_gpus": ws,
+                           "ms_fwd": ms, "elements_per_s": 64 * N / (ms * 1e-3),
+                           "collective": "none"}
+        del x, y
+        torch.cuda.empty_cache()
+    except Exception as exc:
+        res["c3_split"] = {"error": str(exc)[:300]}
+    try:
+        k, K = 8, 16
+        N1 = N2 = 1 << 12
+        N = N1 * N2
+        params = gp.GfpParams(R[k], k)
+        field = gp.GfpFftField(params, backend="cuda")
+        ops = GpuShardOps(field, K, N1, N2, gp.roots_for(params, N))
+        group = None
+        sh = ShardedFFT(ops, k, N1, N2, rank, ws, group)
+        cols = gp.vec.uniform(N1, params, seed=400 + rank, batch=N2 // ws)
+        t = timed_loop(lambda: sh.forward(cols), steps, 2, ws, flush, stream)
+        ms = max_over_ranks(sum(t) / len(t), ws)
+        rows = sh.forward(cols)
+        ok = bool((sh.inverse(rows).view(torch.int64) == cols.view(torch.int64)).all().item())
+        res["c4_sharded"] = {"workload": "C4 fwd k=8 N=2^24 four-step 2^12 x 2^12",
+                             "n_gpus": ws, "ms_fwd": ms, "elements_per_s": N / (ms * 1e-3),
+                             "collective": "NCCL all_to_all_single x1" if ws > 1 else "none",
+                             "roundtrip_exact": ok, "scaling": "strong"}
+        del cols, rows
+        torch.cuda.empty_cache()
+    except Exception as exc:
+        res["c4_sharded"] = {"error": str(exc)[:300]}
+    return res
 
 
 def extra_configs(args, dev, flush, stream):

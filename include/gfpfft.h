@@ -139,6 +139,15 @@ int gfp_fft_exec_host(gfp_fft_plan *plan, uint64_t *v, int64_t batch, int invers
 int gfp_poly_mul_host(gfp_fft_plan *plan, const uint64_t *f, const uint64_t *g, uint64_t *out,
                       int64_t batch, void *stream);
 
+/* Four-step inter-stage twiddle of the sharded transform: x is canonical
+   digit-major [batch][k][n]; element (b, i) is multiplied by
+   omega^((row0 + b) * i) (omega^-((row0 + b) * i) if inverse), omega the
+   plan's N-th root (exponents taken mod N).  Canonical output; out may
+   equal x.  (The reference has no distributed transform;
+   this is the D_{N1,N2} stage of its tensor formula, fft.py:62-103.) */
+int gfp_fft_twiddle(const gfp_fft_plan *plan, const uint64_t *x, uint64_t *out, int64_t batch,
+                    int64_t n, int64_t row0, int inverse, void *stream);
+
 /* Number of kernel launches issued by the last exec/poly_mul call on this
    plan (instrumentation for the benchmark's gpu_launches count). */
 int64_t gfp_fft_plan_last_launches(const gfp_fft_plan *plan);

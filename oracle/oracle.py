@@ -57,6 +57,7 @@ def lib():
         L.orc_poly_mul.argtypes = [ctypes.c_void_p, _u64p, _u64p, _u64p, c_int]
         L.orc_is_canonical.argtypes = [_u64p, i64, c_int, u64,
                                        ctypes.POINTER(ctypes.c_uint8)]
+        L.orc_plan_table.argtypes = [ctypes.c_void_p, _u64p, i64]
         _lib = L
     return _lib
 
@@ -153,6 +154,13 @@ class Plan:
         if not self._h:
             raise ValueError("oracle build_plan rejected the parameters (code %d)"
                              % err.value)
+
+    def table(self, n=None):
+        """omega^j for j < n <= N/K (FftPlan.twiddle_table, fft.py:211-214)."""
+        n = self.N // self.K if n is None else n
+        out = np.zeros((n, self.k), dtype=np.uint64)
+        _check(lib().orc_plan_table(self._h, _p(out), n), "plan table")
+        return out
 
     def prepare_inverse(self):
         _check(lib().orc_plan_prepare_inverse(self._h), "inverse plan")

@@ -665,6 +665,72 @@ __global__ void k_table_balance(u64 *__restrict__ tab, int64_t n, u64 r)
     }
 }
 
+// Four-step inter-stage twiddle (the sharded transform):
+// x is digit-major [batch][k][n] canonical; element (b, i) is multiplied by
+// omega^((row0 + b) i) (omega^-(...) when inverse), omega the plan's N-th
+// root, using the plan's table omega^j (j < N/K) and the cheap split
+// omega^E = (omega^(N/K))^a omega^j as a digit rotation.  Canonical output.
+template <int KD, bool SPARSE>
+__global__ void k_twiddle_rows(const u64 *__restrict__ x, u64 *__restrict__ out,
+                               const u64 *__restrict__ table, int64_t batch, int64_t n,
+                               int64_t row0, int lN, int lM, int inverse, int root_inv,
+                               RadixConsts rc)
+{
+    const int64_t total = batch * n;
+    const int64_t N = (int64_t)1 << lN, M = (int64_t)1 << lM;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = t / n, i = t - b * n;
+        const u64 *src = x + b * KD * n + i;
+        u64 *dst = out + b * KD * n + i;
+        i64 v[KD];
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            v[d] = (i64)src[d * n];
+        int64_t E = ((row0 + b) * i) & (N - 1);
+        if (inverse && E)
+            E = N - E;
+        int a = (int)(E >> lM);
+        const int64_t j = E & (M - 1);
+        if (root_inv && a)
+            a = 2 * KD - a;
+        if (j) {
+            i64 y[KD];
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                y[d] = (i64)table[j * KD + d];
+            to_balanced<KD>(v, rc.r);
+            fast_mul_lazy<KD, SPARSE>(v, y, v, rc);
+        }
+        // rotation by a with the wrapped digits negated (r^k = -1), as a
+        // log-depth network of compile-time rotations (no local memory)
+        i64 w[KD];
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            w[d] = v[d];
+#pragma unroll
+        for (int s = 1; s < 2 * KD; s <<= 1) {
+            const bool on = (a & s) != 0;
+            i64 rot[KD];
+#pragma unroll
+            for (int d = 0; d < KD; d++) {
+                if (s == KD)
+                    rot[d] = -w[d];
+                else
+                    rot[d] = d >= s ? w[d - s] : -w[d - s + KD];
+            }
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                w[d] = on ? rot[d] : w[d];
+        }
+        u64 c[KD];
+        lazy_to_canonical(w, c, KD, rc);
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            dst[d * n] = c[d];
+    }
+}
+
 // ===========================================================================
 // C-ABI
 // ===========================================================================
@@ -1156,6 +1222,26 @@ int gfp_fft_plan_create(gfp_fft_plan **plan, int k, uint64_t r, int K, int e,
     }
     *plan = p;
     return GFP_OK;
+}
+
+int gfp_fft_twiddle(const gfp_fft_plan *p, const uint64_t *x, uint64_t *out, int64_t batch,
+                    int64_t n, int64_t row0, int inverse, void *stream)
+{
+    if (!p || !x || !out || batch < 1 || n < 1 || row0 < 0)
+        return GFP_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int lN = ilog2_exact(p->N), lM = ilog2_exact(p->M);
+    dim3 grid = grid_for(batch * n, 128);
+    if (p->rc.sp_on) {
+        DISPATCH_FAST_K(p->k, (k_twiddle_rows<KD, true><<<grid, 128, 0, st>>>(
+                                  x, out, p->table, batch, n, row0, lN, lM, inverse ? 1 : 0,
+                                  p->root_inv, p->rc)));
+    } else {
+        DISPATCH_FAST_K(p->k, (k_twiddle_rows<KD, false><<<grid, 128, 0, st>>>(
+                                  x, out, p->table, batch, n, row0, lN, lM, inverse ? 1 : 0,
+                                  p->root_inv, p->rc)));
+    }
+    return cuda_status();
 }
 
 int gfp_fft_plan_destroy(gfp_fft_plan *p)
