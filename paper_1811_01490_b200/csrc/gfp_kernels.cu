@@ -382,7 +382,10 @@ struct PassArgs {
     u64 *out;
     const u64 *table;  // element-major [M][k] canonical, omega^b (or omega^b / N)
     const u64 *pre;    // optional pointwise operand, digit-major like `in`
+    const u64 *in2;    // optional second set of `batch` vectors (grid.y >= batch)
+    u64 *out2;
     int64_t batch_stride;
+    int64_t batch;
     int lN, lM, lNs;   // log2 of N, M = N/K and Ns (all powers of two)
     int lG;            // log2 of the groups per CTA
     int neg_exp;   // twiddle exponent N - E (inverse transform)
@@ -442,13 +445,22 @@ __global__ void __launch_bounds__(256) k_pass(PassArgs A)
     const int lG = A.lG;
     const int G = 1 << lG;
     const int tid = threadIdx.x;
-    const int64_t bidx = blockIdx.y;
+    // grid.y covers `batch` vectors of (in, out) and then, when in2 is set,
+    // `batch` more of (in2, out2): two independent transforms in one launch
+    int64_t bidx = blockIdx.y;
+    const u64 *in_base = A.in;
+    u64 *out_base = A.out;
+    if (bidx >= A.batch) {
+        bidx -= A.batch;
+        in_base = A.in2;
+        out_base = A.out2;
+    }
     const int64_t j0 = (int64_t)blockIdx.x << lG;
     const int lN = A.lN, lM = A.lM, lNs = A.lNs;
     const int64_t N = (int64_t)1 << lN, M = (int64_t)1 << lM;
     const int64_t nsmask = ((int64_t)1 << lNs) - 1;
-    const u64 *in = A.in + bidx * A.batch_stride;
-    u64 *out = A.out + bidx * A.batch_stride;
+    const u64 *in = in_base + bidx * A.batch_stride;
+    u64 *out = out_base + bidx * A.batch_stride;
     const u64 *pre = A.pre ? A.pre + bidx * A.batch_stride : nullptr;
     const RadixConsts rc = A.rc;
 
@@ -1001,9 +1013,9 @@ static size_t pass_smem(int G)
 }
 
 template <int KD>
-static int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *pre,
-                       int64_t batch, int64_t Ns, int inverse, int scale, int canon,
-                       int in_canon, cudaStream_t st)
+static int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
+                       u64 *out2, const u64 *pre, int64_t batch, int64_t Ns, int inverse,
+                       int scale, int canon, int in_canon, cudaStream_t st)
 {
     int G;
     int threads = pass_threads(KD, p->M, &G);
@@ -1033,50 +1045,73 @@ static int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64
     A.canon = canon;
     A.in_canon = in_canon;
     A.rc = p->rc;
-    dim3 grid((unsigned)((p->M + G - 1) / G), (unsigned)batch);
-    if (p->rc.sp_on)
+    A.in2 = in2;
+    A.out2 = out2;
+    A.batch = batch;
+    dim3 grid((unsigned)((p->M + G - 1) / G), (unsigned)(in2 ? 2 * batch : batch));
+    if (p->rc.sp_on) {
         k_pass<KD, true><<<grid, threads, smem, st>>>(A);
-    else
+    } else {
         k_pass<KD, false><<<grid, threads, smem, st>>>(A);
+    }
     return cuda_status();
 }
 
-// One transform of `batch` vectors.  in_canon: the input is canonical
-// (user data) and is converted to balanced digits on load; out_canon: the
-// last pass canonicalises (user-visible output) -- poly_mul keeps its
-// intermediate spectra as balanced lazy digits.  `pre` is a pointwise
-// operand (balanced lazy) multiplied in on the first pass.
-static int run_transform(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, const u64 *pre,
-                         int64_t batch, int inverse, int in_canon, int out_canon,
-                         cudaStream_t st)
+// One transform of `batch` vectors (and, when in_b is given, a second
+// independent set of `batch` vectors transformed in the same launches).
+// in_canon: the input is canonical (user data) and is converted to balanced
+// digits on load; out_canon: the last pass canonicalises (user-visible
+// output) -- poly_mul keeps its intermediate spectra as balanced lazy digits.
+// `pre` is a pointwise operand (balanced lazy) multiplied in on the first
+// pass (single set only).
+static int run_transform2(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, const u64 *in_b,
+                          u64 *out_b, u64 *work_b, const u64 *pre, int64_t batch, int inverse,
+                          int in_canon, int out_canon, cudaStream_t st)
 {
-    // ping-pong so that the last pass lands in `out`; `in` is never written
+    // ping-pong so that the last pass lands in `out`; inputs are never written
     int e = p->e;
-    const u64 *src = in;
+    const u64 *src = in, *src_b = in_b;
     int64_t Ns = 1;
     for (int pass = 0; pass < e; pass++) {
         int remaining = e - pass;  // passes left including this one
         u64 *dst = (remaining % 2 == 1) ? out : work;
         if (dst == src)
             dst = (dst == out) ? work : out;
+        u64 *dst_b = nullptr;
+        if (in_b) {
+            dst_b = (remaining % 2 == 1) ? out_b : work_b;
+            if (dst_b == src_b)
+                dst_b = (dst_b == out_b) ? work_b : out_b;
+        }
         int last = pass == e - 1;
         int scale = inverse && last;
         const u64 *pre_p = pass == 0 ? pre : nullptr;
         int rcode;
-        DISPATCH_FAST_K(p->k, (rcode = launch_pass<KD>(p, src, dst, pre_p, batch, Ns, inverse,
-                                                       scale, last && out_canon,
+        DISPATCH_FAST_K(p->k, (rcode = launch_pass<KD>(p, src, dst, src_b, dst_b, pre_p, batch,
+                                                       Ns, inverse, scale, last && out_canon,
                                                        pass == 0 && in_canon, st)));
         if (rcode)
             return rcode;
         p->last_launches++;
         src = dst;
+        src_b = dst_b;
         Ns *= p->K;
     }
-    if (src != out) {
+    if (src != out)
         cudaMemcpyAsync(out, src, sizeof(u64) * (size_t)p->k * p->N * batch,
                         cudaMemcpyDeviceToDevice, st);
-    }
+    if (in_b && src_b != out_b)
+        cudaMemcpyAsync(out_b, src_b, sizeof(u64) * (size_t)p->k * p->N * batch,
+                        cudaMemcpyDeviceToDevice, st);
     return cuda_status();
+}
+
+static int run_transform(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, const u64 *pre,
+                         int64_t batch, int inverse, int in_canon, int out_canon,
+                         cudaStream_t st)
+{
+    return run_transform2(p, in, out, work, nullptr, nullptr, nullptr, pre, batch, inverse,
+                          in_canon, out_canon, st);
 }
 
 extern "C" {
@@ -1259,7 +1294,7 @@ int64_t gfp_fft_plan_size(const gfp_fft_plan *p) { return p ? p->N : 0; }
 
 int64_t gfp_fft_workspace_words(const gfp_fft_plan *p, int64_t batch)
 {
-    return p ? 2 * (int64_t)p->k * p->N * batch : 0;
+    return p ? 3 * (int64_t)p->k * p->N * batch : 0;
 }
 
 int64_t gfp_fft_plan_last_launches(const gfp_fft_plan *p) { return p ? p->last_launches : 0; }
@@ -1286,10 +1321,10 @@ int gfp_poly_mul(const gfp_fft_plan *cp, const uint64_t *f, const uint64_t *g, u
     int64_t vw = (int64_t)p->k * p->N * batch;
     u64 *G = work;        // DFT(g)
     u64 *scratch = work + vw;
-    // spectra stay balanced lazy digits; only the product is canonicalised
-    int err = run_transform(p, f, out, scratch, nullptr, batch, 0, 1, 0, st);  // out = DFT(f)
-    if (!err)
-        err = run_transform(p, g, G, scratch, nullptr, batch, 0, 1, 0, st);    // G = DFT(g)
+    u64 *scratch_b = work + 2 * vw;
+    // out = DFT(f) and G = DFT(g) in the same launches; the spectra stay
+    // balanced lazy digits, only the product is canonicalised
+    int err = run_transform2(p, f, out, scratch, g, G, scratch_b, nullptr, batch, 0, 1, 0, st);
     if (!err)  // out = IDFT(out .* G), the pointwise product fused into pass 0
         err = run_transform(p, out, out, scratch, G, batch, 1, 0, 1, st);
     return err;
@@ -1341,7 +1376,7 @@ int gfp_poly_mul_host(gfp_fft_plan *p, const uint64_t *f, const uint64_t *g, uin
         return GFP_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     int64_t vw = (int64_t)p->k * p->N * batch;
-    int err = ensure_host_scratch(p, 6 * vw);
+    int err = ensure_host_scratch(p, 7 * vw);
     if (err)
         return err;
     u64 *hf = p->h_dev, *hg = hf + vw, *df = hg + vw, *dg = df + vw, *w = dg + vw;

@@ -1,0 +1,47 @@
+"""A/B timing of library builds: python tools/time_variants.py lib1.so lib2.so ...
+Each library is timed in a fresh subprocess (GFPFFT_LIB) on C2 poly-mul
+(graph replay, L2 flushed), C4 forward and C3 forward (8 transforms)."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r'''
+import json, sys, torch
+sys.path.insert(0, %r)
+import paper_1811_01490_b200 as gp
+from bench import R
+res = {}
+flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+def timeit(fn, reps, warm=3):
+    for _ in range(warm): fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record(); fn(); b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
+    ts.sort(); return ts[len(ts) // 2]
+p8 = gp.GfpParams(R[8], 8); f8 = gp.GfpFftField(p8, backend="cuda")
+plan2 = gp.build_plan(f8, 16, 4, gp.roots_for(p8, 1 << 16))
+f = gp.vec.uniform(1 << 16, p8, seed=1); g = gp.vec.uniform(1 << 16, p8, seed=2)
+out = torch.empty_like(f)
+res["c2_polymul_ms"] = timeit(lambda: gp.poly_mul(f, g, plan2, out=out), 100)
+plan4 = gp.build_plan(f8, 16, 6, gp.roots_for(p8, 1 << 24))
+x = gp.vec.uniform(1 << 24, p8, seed=4); y = torch.empty_like(x)
+res["c4_fwd_ms"] = timeit(lambda: gp.fft_tensor(x, plan4, out=y), 10)
+del x, y
+p16 = gp.GfpParams(R[16], 16); f16 = gp.GfpFftField(p16, backend="cuda")
+plan3 = gp.build_plan(f16, 32, 4, gp.roots_for(p16, 1 << 20))
+x = gp.vec.uniform(1 << 20, p16, seed=3, batch=8); y = torch.empty_like(x)
+res["c3x8_fwd_ms"] = timeit(lambda: gp.fft_tensor(x, plan3, out=y), 10)
+print(json.dumps(res))
+''' % ROOT
+
+for lib in sys.argv[1:]:
+    env = dict(os.environ, GFPFFT_LIB=os.path.abspath(lib))
+    outp = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
+    line = outp.stdout.strip().splitlines()[-1] if outp.stdout.strip() else outp.stderr[-500:]
+    print(os.path.basename(lib), line, flush=True)
