@@ -1,0 +1,571 @@
+// gfp_elem.cu -- element-wise kernels (thread per element, any power-of-two
+// k <= 128, any r), the radix constants and the element-wise C-ABI.
+//
+//   k_add / k_sub / k_mul_pow_r  restate gfp_field.py:82-161 digit loops;
+//   k_mul / k_pow                exact generic multiply (gfp_generic.cuh);
+//   k_mul_fast                   limb-split IMAD.WIDE multiply when eligible.
+#include "gfp_internal.cuh"
+#include "gfp_fast.cuh"
+#include "gfp_generic.cuh"
+
+// ===========================================================================
+// host-side constants
+// ===========================================================================
+
+int ilog2_exact(int64_t v)
+{
+    int l = 0;
+    while (((int64_t)1 << l) < v)
+        l++;
+    return ((int64_t)1 << l) == v ? l : -1;
+}
+
+bool valid_k(int k) { return k >= 1 && k <= 128 && (k & (k - 1)) == 0; }
+
+static int fast_split_for(int k) { return k <= 16 ? 29 : 28; }  // FastSplit<KD>::S
+
+struct FastPlan {
+    int S;        // lazy radix-2 stages between normalisations
+    int sp_on;    // sparse-radix normalisation (r = 2^a + eps, |eps| small)
+    int sp_a;
+    i64 sp_eps;
+    u128 delta;   // balanced lazy digits stay in [-r/2 - delta, r/2 + delta]
+};
+
+// balanced normaliser (norm_bal) on |v| <= V: the quotient bound and the
+// excess it leaves over [-r/2, r/2]
+static void norm_bounds(u128 V, u64 r, const FastPlan &fp, u128 *qmax, u128 *ex)
+{
+    if (fp.sp_on) {
+        u128 q = ((V + ((u128)1 << (fp.sp_a - 1))) >> fp.sp_a) + 1;
+        u128 e = (u128)(fp.sp_eps < 0 ? -fp.sp_eps : fp.sp_eps);
+        *qmax = q;
+        *ex = q * (e + 1) + e / 2 + 2;
+    } else {
+        u128 q = V / r + 2;
+        *qmax = q;
+        *ex = q + 2;
+    }
+}
+
+// Fast-path bound check, exact integer arithmetic.  Returns true and fills
+// `fp` when every bound of fast_mul_lazy (gfp_fast.cuh) and of the lazy
+// butterflies (k_pass) holds for balanced digits |d| <= X = r/2 + delta:
+//   * 2^S X + 2^a < 2^63 (S unnormalised radix-2 stages, then norm_bal);
+//   * the sub-column sums LL, SS, HH (and MID = SS - LL - HH,
+//     MID + (LL >> s)) of the balanced-limb product stay below 2^63;
+//   * k X^2 < 2^63 r (the biased column c + 2^63 r is in [0, 2^64 r));
+//   * the carry rounds stay within 2^63 and land back inside delta.
+static bool fast_bounds(int k, u64 r, FastPlan *out)
+{
+    if (!(k == 4 || k == 8 || k == 16 || k == 32))
+        return false;
+    if (r < ((u64)1 << 24) || r >= ((u64)1 << 62) || (r & (r - 1)) == 0)
+        return false;
+    const u128 two63 = (u128)1 << 63;
+    const int K = 2 * k;
+    const int logK = ilog2_exact(K);
+    const u128 kk = (u128)k;
+    FastPlan fp;
+    memset(&fp, 0, sizeof(fp));
+    // sparse radix: r = 2^a + eps with 2^a the nearest power of two
+    int w = 64 - __builtin_clzll(r);
+    u64 lo_p = (u64)1 << (w - 1);
+    u64 hi_p = (u64)1 << w;
+    if (r - lo_p <= hi_p - r) {
+        fp.sp_a = w - 1;
+        fp.sp_eps = (i64)(r - lo_p);
+    } else {
+        fp.sp_a = w;
+        fp.sp_eps = -(i64)(hi_p - r);
+    }
+    i64 aeps = fp.sp_eps < 0 ? -fp.sp_eps : fp.sp_eps;
+    fp.sp_on = aeps < ((i64)1 << 30) && fp.sp_a >= 40 && (aeps << 20) < ((i64)1 << fp.sp_a);
+    const int s = fast_split_for(k);
+    const u128 half = (u128)1 << (s - 1);
+    const u128 top = (u128)1 << (fp.sp_on ? fp.sp_a : w);
+    u128 delta = 2;  // canonical inputs enter through to_balanced (excess <= 1)
+    for (int iter = 0; iter < 16; iter++) {
+        u128 X = (u128)(r / 2) + delta;
+        int S = 0;
+        for (int t = 1; t <= logK; t++)
+            if ((X << t) + top < two63)
+                S = t;
+        if (S < 1)
+            return false;
+        fp.S = S;
+        u128 q1, ex1;
+        norm_bounds(X << S, r, fp, &q1, &ex1);
+        // multiply: balanced limbs, |xl| <= 2^(s-1), |xh| <= H, |xs| <= 2^(s-1) + H
+        u128 H = (X + half) >> s;
+        u128 Hs = half + H;
+        if (Hs >= ((u128)1 << 31))
+            return false;
+        if (kk * half * half >= two63 || kk * H * H >= two63 || kk * Hs * Hs >= two63)
+            return false;
+        if (2 * kk * half * H + kk * half * half / ((u128)1 << s) + 2 >= two63)
+            return false;
+        if (w < 2 * s && ((kk * H * H) << (2 * s - w)) >= two63)
+            return false;
+        u128 XX = X * X;
+        if (XX / r * kk + kk + 8 >= two63)
+            return false;
+        u128 Q1 = XX / r * kk + kk + 8;  // |column quotient|
+        u128 E = 4 * (u128)r + Q1;       // |rem + carry| after round 1
+        if (E + top >= two63)
+            return false;
+        u128 q2, ex2;
+        norm_bounds(E, r, fp, &q2, &ex2);
+        u128 need = ex1 > ex2 ? ex1 : ex2;
+        if (need <= delta)
+            break;
+        delta = need;
+        if (iter == 15)
+            return false;
+    }
+    if (delta * 8 >= r)
+        return false;
+    fp.delta = delta;
+    *out = fp;
+    return true;
+}
+
+RadixConsts make_consts(int k, u64 r)
+{
+    RadixConsts c;
+    memset(&c, 0, sizeof(c));
+    c.r = r;
+    c.sh = __builtin_clzll(r);
+    c.d_norm = r << c.sh;
+    u128 all = ~(u128)0;
+    u128 v = all / c.d_norm;
+    c.v_recip = (u64)(v - ((u128)1 << 64));
+    u128 bias = (u128)r << 63;
+    c.bias_lo = (u64)bias;
+    c.bias_hi = (u64)(bias >> 64);
+    c.rinv = 1.0 / (double)r;
+    c.w = 64 - c.sh;
+    if (c.w < 64) {
+        u128 m = ((u128)1 << (64 + c.w)) / r;
+        c.m_recip = (u64)(m - ((u128)1 << 64));
+    }
+    FastPlan fp;
+    if (fast_bounds(k, r, &fp)) {
+        c.s = fast_split_for(k);
+        c.stages_per_norm = fp.S;
+        c.sp_on = fp.sp_on;
+        c.sp_a = fp.sp_a;
+        c.sp_eps = (int)fp.sp_eps;
+        c.sp_mask = ((i64)1 << fp.sp_a) - 1;
+        c.sp_half = (i64)1 << (fp.sp_a - 1);
+        c.q_sh1 = c.w > 2 * c.s ? c.w - 2 * c.s : 0;
+        c.q_sh2 = c.w < 2 * c.s ? 2 * c.s - c.w : 0;
+        c.bias_t = r << (63 - c.w);
+    } else {
+        c.s = 0;
+        c.stages_per_norm = 0;
+    }
+    return c;
+}
+
+bool fast_path_bounds_ok(int k, u64 r)
+{
+    FastPlan fp;
+    return fast_bounds(k, r, &fp);
+}
+
+// ===========================================================================
+// element-wise kernels (grid-stride, thread per element)
+// ===========================================================================
+
+template <int KD>
+__global__ void k_add(const u64 *__restrict__ x, const u64 *__restrict__ y, u64 *__restrict__ z,
+                      int64_t n, u64 r, int sub)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        u64 a[KD], b[KD], c[KD];
+#pragma unroll
+        for (int d = 0; d < KD; d++) {
+            a[d] = x[d * n + i];
+            b[d] = y[d * n + i];
+        }
+        if (sub)
+            dev_gfp_sub(a, b, c, KD, r);
+        else
+            dev_gfp_add(a, b, c, KD, r);
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            z[d * n + i] = c[d];
+    }
+}
+
+// gfp_mul_pow_r (gfp_field.py:138-161): i >= k negates first, then
+// B - A with B the up-shifted digits, A the wrapped top digits; a form-B
+// digit r moves one slot up.
+template <int KD>
+__global__ void k_mul_pow_r(const u64 *__restrict__ x, u64 *__restrict__ z, int64_t n, u64 r,
+                            int shift)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        u64 a[KD], A[KD], B[KD];
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            a[d] = x[d * n + i];
+        int s = shift % (2 * KD);
+        if (s >= KD) {
+            u64 zero[KD];
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                zero[d] = 0;
+            dev_gfp_sub(zero, a, a, KD, r);
+            s -= KD;
+        }
+        if (s) {
+            bool formb = a[KD - 1] == r;
+#pragma unroll
+            for (int d = 0; d < KD; d++) {
+                int src = d - s;
+                B[d] = src >= 0 ? a[src] : 0;
+                A[d] = src < 0 ? a[src + KD] : 0;
+            }
+            if (formb) {
+                // a[k-1] = r lands in A[s-1]; carry it one slot up
+                for (int d = 0; d < KD; d++) {
+                    if (d == s - 1)
+                        A[d] -= r;
+                    if (d == s)
+                        A[d] += 1;
+                }
+            }
+            dev_gfp_sub(B, A, a, KD, r);
+        }
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            z[d * n + i] = a[d];
+    }
+}
+
+template <int KD>
+__global__ void k_mul_generic(const u64 *__restrict__ x, const u64 *__restrict__ y, int64_t y_inc,
+                              u64 *__restrict__ z, int64_t n, RadixConsts rc)
+{
+    int64_t yn = y_inc ? n : 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        u64 a[KD], b[KD], c[KD];
+        int64_t iy = y_inc ? i : 0;
+        for (int d = 0; d < KD; d++) {
+            a[d] = x[d * n + i];
+            b[d] = y[d * yn + iy];
+        }
+        gfp_mul_generic<KD>(a, b, c, rc);
+        for (int d = 0; d < KD; d++)
+            z[d * n + i] = c[d];
+    }
+}
+
+template <int KD, bool SPARSE>
+__global__ void k_mul_fast(const u64 *__restrict__ x, const u64 *__restrict__ y, int64_t y_inc,
+                           u64 *__restrict__ z, int64_t n, RadixConsts rc)
+{
+    int64_t yn = y_inc ? n : 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        i64 a[KD], b[KD], f[KD];
+        u64 c[KD];
+        int64_t iy = y_inc ? i : 0;
+#pragma unroll
+        for (int d = 0; d < KD; d++) {
+            a[d] = (i64)x[d * n + i];
+            b[d] = (i64)y[d * yn + iy];
+        }
+        to_balanced<KD>(a, rc.r);
+        to_balanced<KD>(b, rc.r);
+        fast_mul_lazy<KD, SPARSE>(a, b, f, rc);
+        lazy_to_canonical(f, c, KD, rc);
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            z[d * n + i] = c[d];
+    }
+}
+
+template <int KD>
+__global__ void k_pow(const u64 *__restrict__ x, const u64 *__restrict__ e, int nbits,
+                      u64 *__restrict__ z, int64_t n, RadixConsts rc)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        u64 a[KD], c[KD];
+        for (int d = 0; d < KD; d++)
+            a[d] = x[d * n + i];
+        gfp_pow_generic<KD>(a, e, nbits, c, rc);
+        for (int d = 0; d < KD; d++)
+            z[d * n + i] = c[d];
+    }
+}
+
+__global__ void k_is_canonical(const u64 *__restrict__ x, uint8_t *__restrict__ out, int64_t n,
+                               int k, u64 r)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        bool all = true, lowzero = true;
+        for (int d = 0; d < k; d++) {
+            u64 v = x[d * n + i];
+            if (v >= r)
+                all = false;
+            if (d < k - 1 && v)
+                lowzero = false;
+        }
+        out[i] = (all || (lowzero && x[(int64_t)(k - 1) * n + i] == r)) ? 1 : 0;
+    }
+}
+
+GFP_D u64 splitmix64(u64 z)
+{
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_uniform(u64 *__restrict__ z, int64_t n, int k, u64 r, u64 seed)
+{
+    int64_t total = n * k;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        u64 h = splitmix64(seed * 0x2545F4914F6CDD1DULL + (u64)t);
+        z[t] = __umul64hi(h, r);  // uniform in [0, r)
+    }
+}
+
+// element-major [n][k] -> digit-major [k][n] (dir = 0) or back (dir = 1)
+__global__ void k_transpose(const u64 *__restrict__ src, u64 *__restrict__ dst, int64_t n, int k,
+                            int dir)
+{
+    int64_t total = n * k;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        // t indexes the destination linearly for coalesced stores
+        if (dir == 0) {
+            int64_t d = t / n, i = t % n;
+            dst[t] = src[i * k + d];
+        } else {
+            int64_t i = t / k, d = t % k;
+            dst[t] = src[d * n + i];
+        }
+    }
+}
+
+static int g_num_sms = 0;
+
+int num_sms()
+{
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0)
+            g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+dim3 grid_for(int64_t work, int threads)
+{
+    int64_t blocks = (work + threads - 1) / threads;
+    int64_t cap = (int64_t)num_sms() * 32;
+    if (blocks > cap)
+        blocks = cap;
+    if (blocks < 1)
+        blocks = 1;
+    return dim3((unsigned)blocks);
+}
+
+int cuda_status()
+{
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? GFP_OK : GFP_ECUDA;
+}
+
+
+extern "C" {
+
+const char *gfp_strerror(int code)
+{
+    switch (code) {
+    case GFP_OK: return "ok";
+    case GFP_EINVAL: return "invalid argument";
+    case GFP_ECONFIG: return "configuration not supported by the prime pair";
+    case GFP_ECUDA: return "CUDA runtime error";
+    case GFP_ENOMEM: return "device allocation failed";
+    case GFP_EUNSUPPORTED: return "parameters outside the transform kernels' range";
+    default: return "unknown error";
+    }
+}
+
+int gfp_version(void) { return 1; }
+
+int gfp_check_prime_compat(int k, uint64_t r)
+{
+    const u64 P1 = 4179340454199820289ULL, P2 = 2485986994308513793ULL;
+    if (!valid_k(k) || r < 2)
+        return 0;
+    u128 limit = ((u128)P1 * P2 - 1) / 2;
+    u128 r2 = (u128)r * r;
+    if (r2 > limit / (u64)k)
+        return 0;
+    if ((P1 - 1) % (2 * (u64)k) || (P2 - 1) % (2 * (u64)k))
+        return 0;
+    return 1;
+}
+
+int gfp_fast_path_ok(int k, uint64_t r)
+{
+    return fast_path_bounds_ok(k, r) ? 1 : 0;
+}
+
+}  // extern "C"
+
+int check_kr(int k, u64 r)
+{
+    if (!valid_k(k) || r < 2)
+        return GFP_EINVAL;
+    return GFP_OK;
+}
+
+extern "C" {
+
+int gfp_vec_add(const uint64_t *x, const uint64_t *y, uint64_t *z, int64_t n, int k, uint64_t r,
+                void *stream)
+{
+    int e = check_kr(k, r);
+    if (e || n <= 0)
+        return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    DISPATCH_K(k, (k_add<KD><<<grid_for(n, 256), 256, 0, st>>>(x, y, z, n, r, 0)));
+    return cuda_status();
+}
+
+int gfp_vec_sub(const uint64_t *x, const uint64_t *y, uint64_t *z, int64_t n, int k, uint64_t r,
+                void *stream)
+{
+    int e = check_kr(k, r);
+    if (e || n <= 0)
+        return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    DISPATCH_K(k, (k_add<KD><<<grid_for(n, 256), 256, 0, st>>>(x, y, z, n, r, 1)));
+    return cuda_status();
+}
+
+int gfp_vec_mul_pow_r(const uint64_t *x, uint64_t *z, int64_t n, int k, uint64_t r, int i,
+                      void *stream)
+{
+    int e = check_kr(k, r);
+    if (e)
+        return e;
+    if (i < 0 || i > 2 * k)
+        return GFP_EINVAL;
+    if (n <= 0)
+        return GFP_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    DISPATCH_K(k, (k_mul_pow_r<KD><<<grid_for(n, 256), 256, 0, st>>>(x, z, n, r, i)));
+    return cuda_status();
+}
+
+int gfp_vec_mul(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z, int64_t n,
+                int k, uint64_t r, void *stream)
+{
+    int e = check_kr(k, r);
+    if (e || n <= 0)
+        return e;
+    cudaStream_t st = (cudaStream_t)stream;
+    RadixConsts rc = make_consts(k, r);
+    if (rc.stages_per_norm > 0) {
+        if (rc.sp_on) {
+            DISPATCH_FAST_K(k, (k_mul_fast<KD, true><<<grid_for(n, 128), 128, 0, st>>>(
+                                   x, y, y_inc, z, n, rc)));
+        } else {
+            DISPATCH_FAST_K(k, (k_mul_fast<KD, false><<<grid_for(n, 128), 128, 0, st>>>(
+                                   x, y, y_inc, z, n, rc)));
+        }
+    } else {
+        DISPATCH_K(k, (k_mul_generic<KD><<<grid_for(n, 128), 128, 0, st>>>(x, y, y_inc, z, n,
+                                                                           rc)));
+    }
+    return cuda_status();
+}
+
+int gfp_vec_pow(const uint64_t *x, const uint64_t *e_limbs, int e_nlimbs, uint64_t *z, int64_t n,
+                int k, uint64_t r, void *stream)
+{
+    int e = check_kr(k, r);
+    if (e)
+        return e;
+    if (n <= 0)
+        return GFP_OK;
+    if (e_nlimbs < 0)
+        return GFP_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    int nl = e_nlimbs > 0 ? e_nlimbs : 1;
+    u64 *d_e = nullptr;
+    if (cudaMallocAsync(&d_e, sizeof(u64) * nl, st) != cudaSuccess)
+        return GFP_ENOMEM;
+    u64 zero = 0;
+    cudaMemcpyAsync(d_e, e_nlimbs ? e_limbs : &zero, sizeof(u64) * nl, cudaMemcpyHostToDevice, st);
+    int nbits = 0;
+    for (int i = e_nlimbs - 1; i >= 0; i--)
+        if (e_limbs[i]) {
+            nbits = 64 * i + 64 - __builtin_clzll(e_limbs[i]);
+            break;
+        }
+    RadixConsts rc = make_consts(k, r);
+    DISPATCH_K(k, (k_pow<KD><<<grid_for(n, 64), 64, 0, st>>>(x, d_e, nbits, z, n, rc)));
+    int rcode = cuda_status();
+    cudaStreamSynchronize(st);  // e_limbs is caller host memory
+    cudaFreeAsync(d_e, st);
+    return rcode;
+}
+
+int gfp_vec_is_canonical(const uint64_t *x, uint8_t *out, int64_t n, int k, uint64_t r,
+                         void *stream)
+{
+    int e = check_kr(k, r);
+    if (e || n <= 0)
+        return e;
+    k_is_canonical<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, out, n, k, r);
+    return cuda_status();
+}
+
+int gfp_vec_uniform(uint64_t *z, int64_t n, int k, uint64_t r, uint64_t seed, void *stream)
+{
+    int e = check_kr(k, r);
+    if (e || n <= 0)
+        return e;
+    k_uniform<<<grid_for(n * k, 256), 256, 0, (cudaStream_t)stream>>>(z, n, k, r, seed);
+    return cuda_status();
+}
+
+int gfp_to_digit_major(const uint64_t *src, uint64_t *dst, int64_t n, int k, void *stream)
+{
+    if (!valid_k(k))
+        return GFP_EINVAL;
+    if (n <= 0)
+        return GFP_OK;
+    k_transpose<<<grid_for(n * k, 256), 256, 0, (cudaStream_t)stream>>>(src, dst, n, k, 0);
+    return cuda_status();
+}
+
+int gfp_to_element_major(const uint64_t *src, uint64_t *dst, int64_t n, int k, void *stream)
+{
+    if (!valid_k(k))
+        return GFP_EINVAL;
+    if (n <= 0)
+        return GFP_OK;
+    k_transpose<<<grid_for(n * k, 256), 256, 0, (cudaStream_t)stream>>>(src, dst, n, k, 1);
+    return cuda_status();
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+// gfp_internal.cuh -- declarations shared by the translation units of
+// libgfpfft.so (host helpers, the pass-kernel arguments, the plan object).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "gfp_device.cuh"
+#include "gfpfft.h"
+
+#define FULL_MASK 0xffffffffu
+
+int ilog2_exact(int64_t v);
+bool valid_k(int k);
+RadixConsts make_consts(int k, u64 r);
+bool fast_path_bounds_ok(int k, u64 r);
+int num_sms();
+dim3 grid_for(int64_t work, int threads);
+int cuda_status();
+int check_kr(int k, u64 r);
+
+struct PassArgs {
+    const u64 *in;
+    u64 *out;
+    const u64 *table;  // element-major [M][k] canonical, omega^b (or omega^b / N)
+    const u64 *pre;    // optional pointwise operand, digit-major like `in`
+    const u64 *in2;    // optional second set of `batch` vectors (grid.y >= batch)
+    u64 *out2;
+    int64_t batch_stride;
+    int64_t batch;
+    int lN, lM, lNs;   // log2 of N, M = N/K and Ns (all powers of two)
+    int lG;            // log2 of the groups per CTA
+    int neg_exp;   // twiddle exponent N - E (inverse transform)
+    int rot_inv;   // base-case root of this execution is 1/r (rotations by r^-t)
+    int root_inv;  // the plan's omega^M is 1/r (twiddle split r^-a omega^b)
+    int scale;     // every element gets a table multiply (N^-1 folded in)
+    int canon;     // canonical output (last pass)
+    int in_canon;  // input digits are canonical (convert to balanced on load)
+    RadixConsts rc;
+};
+
+// ---------------------------------------------------------------------------
+// plans
+
+struct gfp_fft_plan {
+    int k, K, e;
+    int64_t N, M;
+    u64 r;
+    RadixConsts rc;
+    u64 *table;       // element-major [M][k]: omega^b
+    u64 *table_ninv;  // element-major [M][k]: omega^b * N^-1
+    // host-path scratch
+    u64 *h_dev;
+    int64_t h_words;
+    int64_t last_launches;
+    int root_inv;  // omega^(N/2k) == 1/r (a plan built on an inverse root)
+};
+
+// one radix-K Stockham pass (gfp_pass.cuh), instantiated per k in gfp_pass_k*.cu
+template <int KD>
+int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2, u64 *out2,
+                const u64 *pre, int64_t batch, int64_t Ns, int inverse, int scale, int canon,
+                int in_canon, cudaStream_t st);
+
+#define DISPATCH_K(k, CALL)                                                                     \
+    switch (k) {                                                                                \
+    case 1: { constexpr int KD = 1; CALL; } break;                                              \
+    case 2: { constexpr int KD = 2; CALL; } break;                                              \
+    case 4: { constexpr int KD = 4; CALL; } break;                                              \
+    case 8: { constexpr int KD = 8; CALL; } break;                                              \
+    case 16: { constexpr int KD = 16; CALL; } break;                                            \
+    case 32: { constexpr int KD = 32; CALL; } break;                                            \
+    case 64: { constexpr int KD = 64; CALL; } break;                                            \
+    case 128: { constexpr int KD = 128; CALL; } break;                                          \
+    default: return GFP_EINVAL;                                                                 \
+    }
+
+#define DISPATCH_FAST_K(k, CALL)                                                                \
+    switch (k) {                                                                                \
+    case 4: { constexpr int KD = 4; CALL; } break;                                              \
+    case 8: { constexpr int KD = 8; CALL; } break;                                              \
+    case 16: { constexpr int KD = 16; CALL; } break;                                            \
+    case 32: { constexpr int KD = 32; CALL; } break;                                            \
+    default: return GFP_EUNSUPPORTED;                                                           \
+    }

@@ -1,0 +1,290 @@
+// gfp_pass.cuh -- the transform's pass kernel (k_pass) and its launcher.
+//
+// k_pass  one radix-K Stockham pass: coalesced digit-row loads, the
+//         general twiddle (or pointwise / N^-1) multiply in registers,
+//         the r^a part of the twiddle folded into the shared-memory store
+//         as a digit rotation, the K-point DFT at root r (or 1/r) as
+//         lazy radix-2 butterflies with one digit per lane (rotations by
+//         r^t are warp shuffles + sign flips), and the store in natural
+//         Stockham order.  The last pass canonicalises.
+#pragma once
+#include "gfp_internal.cuh"
+#include "gfp_fast.cuh"
+
+template <int KD>
+GFP_D i64 rot_lane(i64 val, int t, int d, bool inverse)
+{
+    // multiply the digit vector held one-digit-per-lane by r^t (forward) or
+    // r^-t (inverse), 0 < t < k: a rotation with the wrapped digits negated
+    int src = inverse ? ((d + t) & (KD - 1)) : ((d - t) & (KD - 1));
+    i64 v = __shfl_sync(FULL_MASK, val, src, KD);
+    bool neg = inverse ? (d + t >= KD) : (d < t);
+    return neg ? -v : v;
+}
+
+// one lazy normalisation of a digit held one-digit-per-lane: the quotient
+// moves one lane up (negated into digit 0: r^k = -1)
+template <int KD, bool SPARSE>
+GFP_D void normalize_lane(i64 &v, int d, const RadixConsts &rc)
+{
+    i64 rem;
+    int q = norm_bal<SPARSE>(v, rc, rem);
+    int qin = __shfl_sync(FULL_MASK, q, (d - 1) & (KD - 1), KD);
+    v = rem + (d == 0 ? -qin : qin);
+}
+
+template <int K>
+__host__ __device__ constexpr int bitrev_c(int x)
+{
+    int y = 0;
+    for (int b = 1; b < K; b <<= 1) {
+        y = (y << 1) | (x & 1);
+        x >>= 1;
+    }
+    return y;
+}
+
+// One radix-K Stockham pass over `batch` vectors (grid.y), G = 2^lG groups
+// of K elements per CTA.  Group j reads x[j + t M] (t < K), multiplies by
+// omega^E, E = t (j mod Ns) (M / Ns), and writes the K-point DFT to
+// (j / Ns) Ns K + (j mod Ns) + u Ns.  After log_K N passes the output is the
+// natural-order DFT (the reference's dft_general result, fft.py:298-360).
+template <int KD, bool SPARSE>
+__global__ void __launch_bounds__(256) k_pass(PassArgs A)
+{
+    constexpr int K = 2 * KD;
+    constexpr int LK = KD == 4 ? 3 : KD == 8 ? 4 : KD == 16 ? 5 : 6;
+    constexpr int ROW = KD + 1;  // padded smem row (bank spread)
+    extern __shared__ i64 sm[];  // [K][G][ROW]
+    const int lG = A.lG;
+    const int G = 1 << lG;
+    const int tid = threadIdx.x;
+    // grid.y covers `batch` vectors of (in, out) and then, when in2 is set,
+    // `batch` more of (in2, out2): two independent transforms in one launch
+    int64_t bidx = blockIdx.y;
+    const u64 *in_base = A.in;
+    u64 *out_base = A.out;
+    if (bidx >= A.batch) {
+        bidx -= A.batch;
+        in_base = A.in2;
+        out_base = A.out2;
+    }
+    const int64_t j0 = (int64_t)blockIdx.x << lG;
+    const int lN = A.lN, lM = A.lM, lNs = A.lNs;
+    const int64_t N = (int64_t)1 << lN, M = (int64_t)1 << lM;
+    const int64_t nsmask = ((int64_t)1 << lNs) - 1;
+    const u64 *in = in_base + bidx * A.batch_stride;
+    u64 *out = out_base + bidx * A.batch_stride;
+    const u64 *pre = A.pre ? A.pre + bidx * A.batch_stride : nullptr;
+    const RadixConsts rc = A.rc;
+
+    // ---- phase A: load K elements per group, twiddle / pointwise multiply
+#pragma unroll 1
+    for (int h = 0; h < 2; h++) {
+        const int g = tid & (G - 1);
+        const int t = (tid >> lG) + h * KD;
+        const int64_t j = j0 + g;
+        i64 x[KD];
+        int a = 0;
+        if (j < M) {
+            const int64_t pos = j + ((int64_t)t << lM);
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                x[d] = (i64)__ldg(in + ((int64_t)d << lN) + pos);
+            if (A.in_canon)
+                to_balanced<KD>(x, rc.r);
+            if (pre) {
+                i64 y[KD];
+#pragma unroll
+                for (int d = 0; d < KD; d++)
+                    y[d] = (i64)__ldg(pre + ((int64_t)d << lN) + pos);
+                fast_mul_lazy<KD, SPARSE>(x, y, x, rc);
+            }
+            // E = t (j mod Ns) (M / Ns) < N; omega^E = (omega^M)^a omega^b
+            int64_t E = ((int64_t)t * (j & nsmask)) << (lM - lNs);
+            if (A.neg_exp && E)
+                E = N - E;
+            a = (int)(E >> lM);
+            const int64_t b = E & (M - 1);
+            // omega^M is r (or 1/r for plans built on an inverse root)
+            if (A.root_inv && a)
+                a = 2 * KD - a;
+            if (b || A.scale) {
+                i64 y[KD];
+                const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(A.table + b * KD);
+#pragma unroll
+                for (int d = 0; d < KD; d += 2) {
+                    ulonglong2 w = __ldg(tp + d / 2);
+                    y[d] = (i64)w.x;
+                    y[d + 1] = (i64)w.y;
+                }
+                fast_mul_lazy<KD, SPARSE>(x, y, x, rc);
+            }
+        } else {
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                x[d] = 0;
+        }
+        // x * r^a: rotation by a (0 <= a < 2k), wrapped digits negated
+        i64 *row = sm + (((int64_t)t << lG) + g) * ROW;
+#pragma unroll
+        for (int d = 0; d < KD; d++) {
+            int p = d + a;
+            i64 v = x[d];
+            if (p >= KD) {
+                p -= KD;
+                v = -v;
+            }
+            if (p >= KD) {
+                p -= KD;
+                v = -v;
+            }
+            row[p] = v;
+        }
+    }
+    __syncthreads();
+
+    // ---- phase B: K-point DFT at root r (or 1/r), one digit per lane
+    {
+        const int d = tid & (KD - 1);
+        const int g = tid / KD;
+        const bool inv = A.rot_inv != 0;
+        i64 v[K];
+#pragma unroll
+        for (int t = 0; t < K; t++)
+            v[t] = sm[(((int64_t)t << lG) + g) * ROW + d];
+        const int S = rc.stages_per_norm;
+        int stage = 0;
+#pragma unroll
+        for (int len = K / 2; len >= 1; len >>= 1) {
+#pragma unroll
+            for (int st = 0; st < K; st += 2 * len) {
+#pragma unroll
+                for (int i = 0; i < len; i++) {
+                    i64 a0 = v[st + i], b0 = v[st + i + len];
+                    v[st + i] = a0 + b0;
+                    i64 df = a0 - b0;
+                    const int tw = i * (K / (2 * len));  // exponent of the root, < k
+                    v[st + i + len] = tw ? rot_lane<KD>(df, tw, d, inv) : df;
+                }
+            }
+            stage++;
+            if (len > 1 && stage % S == 0) {
+#pragma unroll
+                for (int t = 0; t < K; t++)
+                    normalize_lane<KD, SPARSE>(v[t], d, rc);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < K; t++)
+            normalize_lane<KD, SPARSE>(v[t], d, rc);
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < K; t++)
+            sm[(((int64_t)bitrev_c<K>(t) << lG) + g) * ROW + d] = v[t];
+    }
+    __syncthreads();
+
+    // ---- phase C: store in Stockham order (canonicalise on the last pass)
+#pragma unroll 1
+    for (int h = 0; h < 2; h++) {
+        const int g = tid & (G - 1);
+        const int u = (tid >> lG) + h * KD;
+        const int64_t j = j0 + g;
+        if (j >= M)
+            continue;
+        const int64_t pos = ((j >> lNs) << (lNs + LK)) + (j & nsmask) + ((int64_t)u << lNs);
+        const i64 *row = sm + (((int64_t)u << lG) + g) * ROW;
+        if (A.canon) {
+            i64 f[KD];
+            u64 c[KD];
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                f[d] = row[d];
+            lazy_to_canonical(f, c, KD, rc);
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                out[((int64_t)d << lN) + pos] = c[d];
+        } else {
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                out[((int64_t)d << lN) + pos] = (u64)row[d];
+        }
+    }
+}
+
+static int pass_threads(int k, int64_t M, int *G_out)
+{
+    // groups per CTA: as many as fit 256 threads, fewer when the transform
+    // is too small to give every SM two CTAs
+    int Gmax = 256 / k;
+    int Gmin = 32 / k > 0 ? 32 / k : 1;
+    static int g_env = -1;
+    if (g_env < 0) {
+        const char *e = getenv("GFP_PASS_G");  // experiment hook: groups per CTA
+        g_env = e ? atoi(e) : 0;
+    }
+    if (g_env > 0) {
+        int G = g_env * Gmin;
+        if (G > Gmax)
+            G = Gmax;
+        *G_out = G;
+        return G * k;
+    }
+    int G = Gmax;
+    while (G > Gmin && (M + G - 1) / G < 2 * (int64_t)num_sms())
+        G >>= 1;
+    *G_out = G;
+    return G * k;
+}
+
+template <int KD>
+static size_t pass_smem(int G)
+{
+    return (size_t)(2 * KD) * G * (KD + 1) * sizeof(i64);
+}
+
+template <int KD>
+int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
+                       u64 *out2, const u64 *pre, int64_t batch, int64_t Ns, int inverse,
+                       int scale, int canon, int in_canon, cudaStream_t st)
+{
+    int G;
+    int threads = pass_threads(KD, p->M, &G);
+    size_t smem = pass_smem<KD>(G);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_pass<KD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pass_smem<KD>(256 / KD));
+        cudaFuncSetAttribute(k_pass<KD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)pass_smem<KD>(256 / KD));
+        attr_set = true;
+    }
+    PassArgs A;
+    A.in = in;
+    A.out = out;
+    A.table = scale ? p->table_ninv : p->table;
+    A.pre = pre;
+    A.batch_stride = (int64_t)KD * p->N;
+    A.lN = ilog2_exact(p->N);
+    A.lM = ilog2_exact(p->M);
+    A.lNs = ilog2_exact(Ns);
+    A.lG = ilog2_exact(G);
+    A.neg_exp = inverse;
+    A.rot_inv = inverse ^ p->root_inv;
+    A.root_inv = p->root_inv;
+    A.scale = scale;
+    A.canon = canon;
+    A.in_canon = in_canon;
+    A.rc = p->rc;
+    A.in2 = in2;
+    A.out2 = out2;
+    A.batch = batch;
+    dim3 grid((unsigned)((p->M + G - 1) / G), (unsigned)(in2 ? 2 * batch : batch));
+    if (p->rc.sp_on) {
+        k_pass<KD, true><<<grid, threads, smem, st>>>(A);
+    } else {
+        k_pass<KD, false><<<grid, threads, smem, st>>>(A);
+    }
+    return cuda_status();
+}

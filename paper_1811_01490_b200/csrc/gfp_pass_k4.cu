@@ -1,0 +1,6 @@
+// instantiation of the pass kernel for k = 4 (one translation unit per k so
+// the heavy template instantiations compile in parallel)
+#include "gfp_pass.cuh"
+
+template int launch_pass<4>(const gfp_fft_plan *, const u64 *, u64 *, const u64 *, u64 *,
+                             const u64 *, int64_t, int64_t, int, int, int, int, cudaStream_t);

@@ -1,0 +1,494 @@
+// gfp_plan.cu -- transform plans (omega validation, twiddle tables built on
+// the device with the exact multiply), the four-step inter-stage twiddle,
+// transform orchestration (Stockham pass sequence, poly-multiply) and the
+// transform C-ABI.
+#include "gfp_internal.cuh"
+#include "gfp_fast.cuh"
+#include "gfp_generic.cuh"
+
+// power table: out[b] = omega^(b * step) for b < n, element-major [n][k]
+// (one thread per entry, square-and-multiply over the bits of b with the
+// precomputed omega^(2^i step) in `sq`), exact generic multiply.
+template <int KD>
+__global__ void k_power_table(const u64 *__restrict__ sq, int nsq, u64 *__restrict__ out,
+                              int64_t n, RadixConsts rc)
+{
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        u64 acc[KD];
+        for (int d = 0; d < KD; d++)
+            acc[d] = d == 0 ? 1 : 0;
+        for (int i = 0; i < nsq; i++) {
+            if ((b >> i) & 1) {
+                u64 y[KD];
+                for (int d = 0; d < KD; d++)
+                    y[d] = sq[(int64_t)i * KD + d];
+                gfp_mul_generic<KD>(acc, y, acc, rc);
+            }
+        }
+        for (int d = 0; d < KD; d++)
+            out[b * KD + d] = acc[d];
+    }
+}
+
+// sq[i] = omega^(2^i), element-major, single thread (plan time only)
+template <int KD>
+__global__ void k_squarings(const u64 *__restrict__ omega, u64 *__restrict__ sq, int nsq,
+                            RadixConsts rc)
+{
+    if (blockIdx.x || threadIdx.x)
+        return;
+    u64 cur[KD];
+    for (int d = 0; d < KD; d++)
+        cur[d] = omega[d];
+    for (int i = 0; i < nsq; i++) {
+        for (int d = 0; d < KD; d++)
+            sq[(int64_t)i * KD + d] = cur[d];
+        gfp_mul_generic<KD>(cur, cur, cur, rc);
+    }
+}
+
+// element-major table times a constant (element-major [1][k])
+template <int KD>
+__global__ void k_table_scale(const u64 *__restrict__ tab, const u64 *__restrict__ c,
+                              u64 *__restrict__ out, int64_t n, RadixConsts rc)
+{
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        u64 a[KD], y[KD], z[KD];
+        for (int d = 0; d < KD; d++) {
+            a[d] = tab[b * KD + d];
+            y[d] = c[d];
+        }
+        gfp_mul_generic<KD>(a, y, z, rc);
+        for (int d = 0; d < KD; d++)
+            out[b * KD + d] = z[d];
+    }
+}
+
+// element-major canonical table entries -> balanced lazy digits (in place);
+// the transform multiplies balanced operands only
+template <int KD>
+__global__ void k_table_balance(u64 *__restrict__ tab, int64_t n, u64 r)
+{
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        i64 x[KD];
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            x[d] = (i64)tab[b * KD + d];
+        to_balanced<KD>(x, r);
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            tab[b * KD + d] = (u64)x[d];
+    }
+}
+
+// Four-step inter-stage twiddle (the sharded transform):
+// x is digit-major [batch][k][n] canonical; element (b, i) is multiplied by
+// omega^((row0 + b) i) (omega^-(...) when inverse), omega the plan's N-th
+// root, using the plan's table omega^j (j < N/K) and the cheap split
+// omega^E = (omega^(N/K))^a omega^j as a digit rotation.  Canonical output.
+template <int KD, bool SPARSE>
+__global__ void k_twiddle_rows(const u64 *__restrict__ x, u64 *__restrict__ out,
+                               const u64 *__restrict__ table, int64_t batch, int64_t n,
+                               int64_t row0, int lN, int lM, int inverse, int root_inv,
+                               RadixConsts rc)
+{
+    const int64_t total = batch * n;
+    const int64_t N = (int64_t)1 << lN, M = (int64_t)1 << lM;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = t / n, i = t - b * n;
+        const u64 *src = x + b * KD * n + i;
+        u64 *dst = out + b * KD * n + i;
+        i64 v[KD];
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            v[d] = (i64)src[d * n];
+        int64_t E = ((row0 + b) * i) & (N - 1);
+        if (inverse && E)
+            E = N - E;
+        int a = (int)(E >> lM);
+        const int64_t j = E & (M - 1);
+        if (root_inv && a)
+            a = 2 * KD - a;
+        if (j) {
+            i64 y[KD];
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                y[d] = (i64)table[j * KD + d];
+            to_balanced<KD>(v, rc.r);
+            fast_mul_lazy<KD, SPARSE>(v, y, v, rc);
+        }
+        // rotation by a with the wrapped digits negated (r^k = -1), as a
+        // log-depth network of compile-time rotations (no local memory)
+        i64 w[KD];
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            w[d] = v[d];
+#pragma unroll
+        for (int s = 1; s < 2 * KD; s <<= 1) {
+            const bool on = (a & s) != 0;
+            i64 rot[KD];
+#pragma unroll
+            for (int d = 0; d < KD; d++) {
+                if (s == KD)
+                    rot[d] = -w[d];
+                else
+                    rot[d] = d >= s ? w[d - s] : -w[d - s + KD];
+            }
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                w[d] = on ? rot[d] : w[d];
+        }
+        u64 c[KD];
+        lazy_to_canonical(w, c, KD, rc);
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            dst[d * n] = c[d];
+    }
+}
+
+// One transform of `batch` vectors (and, when in_b is given, a second
+// independent set of `batch` vectors transformed in the same launches).
+// in_canon: the input is canonical (user data) and is converted to balanced
+// digits on load; out_canon: the last pass canonicalises (user-visible
+// output) -- poly_mul keeps its intermediate spectra as balanced lazy digits.
+// `pre` is a pointwise operand (balanced lazy) multiplied in on the first
+// pass (single set only).
+static int run_transform2(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, const u64 *in_b,
+                          u64 *out_b, u64 *work_b, const u64 *pre, int64_t batch, int inverse,
+                          int in_canon, int out_canon, cudaStream_t st)
+{
+    // ping-pong so that the last pass lands in `out`; inputs are never written
+    int e = p->e;
+    const u64 *src = in, *src_b = in_b;
+    int64_t Ns = 1;
+    for (int pass = 0; pass < e; pass++) {
+        int remaining = e - pass;  // passes left including this one
+        u64 *dst = (remaining % 2 == 1) ? out : work;
+        if (dst == src)
+            dst = (dst == out) ? work : out;
+        u64 *dst_b = nullptr;
+        if (in_b) {
+            dst_b = (remaining % 2 == 1) ? out_b : work_b;
+            if (dst_b == src_b)
+                dst_b = (dst_b == out_b) ? work_b : out_b;
+        }
+        int last = pass == e - 1;
+        int scale = inverse && last;
+        const u64 *pre_p = pass == 0 ? pre : nullptr;
+        int rcode;
+        DISPATCH_FAST_K(p->k, (rcode = launch_pass<KD>(p, src, dst, src_b, dst_b, pre_p, batch,
+                                                       Ns, inverse, scale, last && out_canon,
+                                                       pass == 0 && in_canon, st)));
+        if (rcode)
+            return rcode;
+        p->last_launches++;
+        src = dst;
+        src_b = dst_b;
+        Ns *= p->K;
+    }
+    if (src != out)
+        cudaMemcpyAsync(out, src, sizeof(u64) * (size_t)p->k * p->N * batch,
+                        cudaMemcpyDeviceToDevice, st);
+    if (in_b && src_b != out_b)
+        cudaMemcpyAsync(out_b, src_b, sizeof(u64) * (size_t)p->k * p->N * batch,
+                        cudaMemcpyDeviceToDevice, st);
+    return cuda_status();
+}
+
+static int run_transform(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, const u64 *pre,
+                         int64_t batch, int inverse, int in_canon, int out_canon,
+                         cudaStream_t st)
+{
+    return run_transform2(p, in, out, work, nullptr, nullptr, nullptr, pre, batch, inverse,
+                          in_canon, out_canon, st);
+}
+
+extern "C" {
+
+int gfp_fft_plan_create(gfp_fft_plan **plan, int k, uint64_t r, int K, int e,
+                        const uint64_t *omega, void *stream)
+{
+    if (!plan)
+        return GFP_EINVAL;
+    *plan = nullptr;
+    int err = check_kr(k, r);
+    if (err)
+        return err;
+    if (K != 8 && K != 16 && K != 32 && K != 64)
+        return GFP_EINVAL;
+    if (e < 1)
+        return GFP_EINVAL;
+    if (K != 2 * k)
+        return GFP_EINVAL;
+    int64_t N = 1;
+    for (int i = 0; i < e; i++) {
+        N *= K;
+        if (N > ((int64_t)1 << 40))
+            return GFP_EINVAL;
+    }
+    for (int d = 0; d < k; d++)
+        if (omega[d] > r)
+            return GFP_EINVAL;
+    RadixConsts rc = make_consts(k, r);
+    if (rc.stages_per_norm <= 0)
+        return GFP_EUNSUPPORTED;
+    cudaStream_t st = (cudaStream_t)stream;
+    gfp_fft_plan *p = (gfp_fft_plan *)calloc(1, sizeof(gfp_fft_plan));
+    if (!p)
+        return GFP_ENOMEM;
+    p->k = k;
+    p->K = K;
+    p->e = e;
+    p->N = N;
+    p->M = N / K;
+    p->r = r;
+    p->rc = rc;
+
+    // ---- validate omega like build_plan (fft.py:250-267): omega^N = 1,
+    // omega^(N/2) = -1, omega^(N/2k) in {r, r^(2k-1)}
+    u64 *d_buf = nullptr;
+    size_t words = (size_t)k * 8;
+    if (cudaMalloc(&d_buf, sizeof(u64) * words) != cudaSuccess) {
+        free(p);
+        return GFP_ENOMEM;
+    }
+    // d_buf: [0] omega (digit-major == element-major for n=1), [1..3] results
+    cudaMemcpyAsync(d_buf, omega, sizeof(u64) * k, cudaMemcpyHostToDevice, st);
+    u64 exps[3] = {(u64)N, (u64)(N / 2), (u64)(N / (2 * k))};
+    for (int i = 0; i < 3; i++) {
+        err = gfp_vec_pow(d_buf, &exps[i], 1, d_buf + (size_t)(i + 1) * k, 1, k, r, stream);
+        if (err)
+            break;
+    }
+    u64 h_res[3 * 128];
+    if (!err && cudaMemcpyAsync(h_res, d_buf + k, sizeof(u64) * 3 * k, cudaMemcpyDeviceToHost,
+                                st) != cudaSuccess)
+        err = GFP_ECUDA;
+    if (!err && cudaStreamSynchronize(st) != cudaSuccess)
+        err = GFP_ECUDA;
+    if (!err) {
+        bool one = true, mone = true, fwd = true, inv = true;
+        for (int d = 0; d < k; d++) {
+            if (h_res[d] != (u64)(d == 0))
+                one = false;
+            if (h_res[k + d] != (d == k - 1 ? r : 0))
+                mone = false;
+            // r as an element: digit 1 = 1 (k >= 2)
+            if (h_res[2 * k + d] != (u64)(d == 1))
+                fwd = false;
+        }
+        // 1/r = r^(2k-1) = -(r^(k-1)) = p - r^(k-1) = (r - 1) r^(k-1) + 1
+        for (int d = 0; d < k; d++) {
+            u64 want = (d == k - 1 ? r - 1 : 0) + (d == 0 ? 1 : 0);
+            if (h_res[2 * k + d] != want)
+                inv = false;
+        }
+        if (!one || !mone || !(fwd || inv))
+            err = GFP_EINVAL;
+        p->root_inv = fwd ? 0 : 1;
+    }
+    if (err) {
+        cudaFree(d_buf);
+        free(p);
+        return err;
+    }
+
+    // ---- twiddle tables: omega^b (b < M) and omega^b * N^-1
+    int nsq = 0;
+    while (((int64_t)1 << nsq) < p->M)
+        nsq++;
+    u64 *d_sq = nullptr;
+    size_t tbytes = sizeof(u64) * (size_t)k * p->M;
+    if (cudaMalloc(&p->table, tbytes) != cudaSuccess ||
+        cudaMalloc(&p->table_ninv, tbytes) != cudaSuccess ||
+        cudaMalloc(&d_sq, sizeof(u64) * (size_t)k * (nsq + 1)) != cudaSuccess) {
+        cudaFree(p->table);
+        cudaFree(p->table_ninv);
+        cudaFree(d_sq);
+        cudaFree(d_buf);
+        free(p);
+        return GFP_ENOMEM;
+    }
+    // N^-1 = -(r^k / N) mod p (N | r^k = p - 1): radix-r long division of
+    // r^k by N on the host, then negation with the canonical subtract
+    u64 q[128], ninv[128], zero[128];
+    {
+        u128 rem = 1;  // digit k of r^k
+        for (int i = k - 1; i >= 0; i--) {
+            u128 cur = rem * r;
+            q[i] = (u64)(cur / (u64)N);
+            rem = cur % (u64)N;
+        }
+        for (int d = 0; d < k; d++)
+            zero[d] = 0;
+        dev_gfp_sub(zero, q, ninv, k, r);
+    }
+    cudaMemcpyAsync(d_buf, ninv, sizeof(u64) * k, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_buf + k, omega, sizeof(u64) * k, cudaMemcpyHostToDevice, st);
+    DISPATCH_FAST_K(k, (k_squarings<KD><<<1, 32, 0, st>>>(d_buf + k, d_sq, nsq, rc)));
+    DISPATCH_FAST_K(k, (k_power_table<KD><<<grid_for(p->M, 64), 64, 0, st>>>(d_sq, nsq, p->table,
+                                                                           p->M, rc)));
+    DISPATCH_FAST_K(k, (k_table_scale<KD><<<grid_for(p->M, 64), 64, 0, st>>>(
+                           p->table, d_buf, p->table_ninv, p->M, rc)));
+    DISPATCH_FAST_K(k, (k_table_balance<KD><<<grid_for(p->M, 128), 128, 0, st>>>(p->table, p->M, r)));
+    DISPATCH_FAST_K(k, (k_table_balance<KD><<<grid_for(p->M, 128), 128, 0, st>>>(p->table_ninv, p->M,
+                                                                                r)));
+    err = cuda_status();
+    if (!err && cudaStreamSynchronize(st) != cudaSuccess)
+        err = GFP_ECUDA;
+    cudaFree(d_sq);
+    cudaFree(d_buf);
+    if (err) {
+        cudaFree(p->table);
+        cudaFree(p->table_ninv);
+        free(p);
+        return err;
+    }
+    *plan = p;
+    return GFP_OK;
+}
+
+int gfp_fft_twiddle(const gfp_fft_plan *p, const uint64_t *x, uint64_t *out, int64_t batch,
+                    int64_t n, int64_t row0, int inverse, void *stream)
+{
+    if (!p || !x || !out || batch < 1 || n < 1 || row0 < 0)
+        return GFP_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int lN = ilog2_exact(p->N), lM = ilog2_exact(p->M);
+    dim3 grid = grid_for(batch * n, 128);
+    if (p->rc.sp_on) {
+        DISPATCH_FAST_K(p->k, (k_twiddle_rows<KD, true><<<grid, 128, 0, st>>>(
+                                  x, out, p->table, batch, n, row0, lN, lM, inverse ? 1 : 0,
+                                  p->root_inv, p->rc)));
+    } else {
+        DISPATCH_FAST_K(p->k, (k_twiddle_rows<KD, false><<<grid, 128, 0, st>>>(
+                                  x, out, p->table, batch, n, row0, lN, lM, inverse ? 1 : 0,
+                                  p->root_inv, p->rc)));
+    }
+    return cuda_status();
+}
+
+int gfp_fft_plan_destroy(gfp_fft_plan *p)
+{
+    if (!p)
+        return GFP_OK;
+    cudaFree(p->table);
+    cudaFree(p->table_ninv);
+    cudaFree(p->h_dev);
+    free(p);
+    return GFP_OK;
+}
+
+int64_t gfp_fft_plan_size(const gfp_fft_plan *p) { return p ? p->N : 0; }
+
+int64_t gfp_fft_workspace_words(const gfp_fft_plan *p, int64_t batch)
+{
+    return p ? 3 * (int64_t)p->k * p->N * batch : 0;
+}
+
+int64_t gfp_fft_plan_last_launches(const gfp_fft_plan *p) { return p ? p->last_launches : 0; }
+
+int gfp_fft_exec(const gfp_fft_plan *cp, const uint64_t *in, uint64_t *out, uint64_t *work,
+                 int64_t batch, int inverse, void *stream)
+{
+    gfp_fft_plan *p = const_cast<gfp_fft_plan *>(cp);
+    if (!p || !in || !out || !work || batch < 1)
+        return GFP_EINVAL;
+    p->last_launches = 0;
+    return run_transform(p, in, out, work, nullptr, batch, inverse ? 1 : 0, 1, 1,
+                         (cudaStream_t)stream);
+}
+
+int gfp_poly_mul(const gfp_fft_plan *cp, const uint64_t *f, const uint64_t *g, uint64_t *out,
+                 uint64_t *work, int64_t batch, void *stream)
+{
+    gfp_fft_plan *p = const_cast<gfp_fft_plan *>(cp);
+    if (!p || !f || !g || !out || !work || batch < 1)
+        return GFP_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    p->last_launches = 0;
+    int64_t vw = (int64_t)p->k * p->N * batch;
+    u64 *G = work;        // DFT(g)
+    u64 *scratch = work + vw;
+    u64 *scratch_b = work + 2 * vw;
+    // out = DFT(f) and G = DFT(g) in the same launches; the spectra stay
+    // balanced lazy digits, only the product is canonicalised
+    int err = run_transform2(p, f, out, scratch, g, G, scratch_b, nullptr, batch, 0, 1, 0, st);
+    if (!err)  // out = IDFT(out .* G), the pointwise product fused into pass 0
+        err = run_transform(p, out, out, scratch, G, batch, 1, 0, 1, st);
+    return err;
+}
+
+static int ensure_host_scratch(gfp_fft_plan *p, int64_t words)
+{
+    if (p->h_words >= words)
+        return GFP_OK;
+    cudaFree(p->h_dev);
+    p->h_dev = nullptr;
+    p->h_words = 0;
+    if (cudaMalloc(&p->h_dev, sizeof(u64) * (size_t)words) != cudaSuccess)
+        return GFP_ENOMEM;
+    p->h_words = words;
+    return GFP_OK;
+}
+
+int gfp_fft_exec_host(gfp_fft_plan *p, uint64_t *v, int64_t batch, int inverse, void *stream)
+{
+    if (!p || !v || batch < 1)
+        return GFP_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t vw = (int64_t)p->k * p->N * batch;
+    int err = ensure_host_scratch(p, 3 * vw);
+    if (err)
+        return err;
+    u64 *a = p->h_dev, *b = a + vw, *w = b + vw;
+    cudaMemcpyAsync(a, v, sizeof(u64) * vw, cudaMemcpyHostToDevice, st);
+    p->last_launches = 0;
+    for (int64_t i = 0; i < batch; i++)
+        gfp_to_digit_major(a + i * p->k * p->N, b + i * p->k * p->N, p->N, p->k, st);
+    err = run_transform(p, b, b, w, nullptr, batch, inverse ? 1 : 0, 1, 1, st);
+    if (err)
+        return err;
+    for (int64_t i = 0; i < batch; i++)
+        gfp_to_element_major(b + i * p->k * p->N, a + i * p->k * p->N, p->N, p->k, st);
+    p->last_launches += 2 * batch;
+    cudaMemcpyAsync(v, a, sizeof(u64) * vw, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess)
+        return GFP_ECUDA;
+    return cuda_status();
+}
+
+int gfp_poly_mul_host(gfp_fft_plan *p, const uint64_t *f, const uint64_t *g, uint64_t *out,
+                      int64_t batch, void *stream)
+{
+    if (!p || !f || !g || !out || batch < 1)
+        return GFP_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t vw = (int64_t)p->k * p->N * batch;
+    int err = ensure_host_scratch(p, 7 * vw);
+    if (err)
+        return err;
+    u64 *hf = p->h_dev, *hg = hf + vw, *df = hg + vw, *dg = df + vw, *w = dg + vw;
+    cudaMemcpyAsync(hf, f, sizeof(u64) * vw, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(hg, g, sizeof(u64) * vw, cudaMemcpyHostToDevice, st);
+    for (int64_t i = 0; i < batch; i++) {
+        gfp_to_digit_major(hf + i * p->k * p->N, df + i * p->k * p->N, p->N, p->k, st);
+        gfp_to_digit_major(hg + i * p->k * p->N, dg + i * p->k * p->N, p->N, p->k, st);
+    }
+    err = gfp_poly_mul(p, df, dg, df, w, batch, st);
+    if (err)
+        return err;
+    for (int64_t i = 0; i < batch; i++)
+        gfp_to_element_major(df + i * p->k * p->N, hf + i * p->k * p->N, p->N, p->k, st);
+    p->last_launches += 3 * batch;
+    cudaMemcpyAsync(out, hf, sizeof(u64) * vw, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess)
+        return GFP_ECUDA;
+    return cuda_status();
+}
+
+}  // extern "C"

@@ -1,5 +1,9 @@
-"""Aggregate an ncu source-page CSV (--print-source cuda,sass) per CUDA line
-for the first profiled kernel: stall samples and executed instructions."""
+"""Aggregate an ncu source-page CSV (--page source --csv --print-source cuda,sass)
+per CUDA source line: stall samples and executed warp instructions.
+
+    ncu -i prof.ncu-rep --page source --csv --print-source cuda,sass > src.csv
+    python tools/ncu_lines.py src.csv [top]
+"""
 import csv
 import sys
 
@@ -8,22 +12,23 @@ top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 cur = None
 out = []
 hdr = None
-seen = set()
 for r in rows:
     if r and r[0] == "File Path":
-        if r[1] in seen:
-            break
-        seen.add(r[1])
         cur = r[1].split("/")[-1]
+        hdr = None
         continue
     if r and r[0] == "Line No":
         hdr = r
+        isamp = hdr.index("Warp Stall Sampling (All Samples)")
+        iinst = hdr.index("Instructions Executed")
         continue
-    if r and r[0] not in ("", "Function Name") and hdr:
+    if r and hdr and r[0].isdigit():
         try:
-            out.append((int(r[4]), int(r[7]), cur, r[0], r[1][:80]))
-        except ValueError:
-            pass
+            s, n = int(r[isamp]), int(r[iinst])
+        except (ValueError, IndexError):
+            continue
+        if s or n:
+            out.append((s, n, cur, r[0], r[1][:90]))
 ts = sum(o[0] for o in out) or 1
 ti = sum(o[1] for o in out) or 1
 print("total stall samples", ts, "warp instructions", ti)

@@ -1,4 +1,4 @@
-"""A/B timing of library builds: python tools/time_variants.py lib1.so lib2.so ...
+"""A/B timing of library builds: python tools/time_variants.py lib1.so lib2.so[:VAR=val,...] ...
 Each library is timed in a fresh subprocess (GFPFFT_LIB) on C2 poly-mul
 (graph replay, L2 flushed), C4 forward and C3 forward (8 transforms)."""
 import json
@@ -40,8 +40,12 @@ res["c3x8_fwd_ms"] = timeit(lambda: gp.fft_tensor(x, plan3, out=y), 10)
 print(json.dumps(res))
 ''' % ROOT
 
-for lib in sys.argv[1:]:
+for spec in sys.argv[1:]:
+    lib, _, envs = spec.partition(":")
     env = dict(os.environ, GFPFFT_LIB=os.path.abspath(lib))
+    for kv in filter(None, envs.split(",")):
+        kk, _, vv = kv.partition("=")
+        env[kk] = vv
     outp = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
     line = outp.stdout.strip().splitlines()[-1] if outp.stdout.strip() else outp.stderr[-500:]
-    print(os.path.basename(lib), line, flush=True)
+    print(spec.replace(os.path.dirname(os.path.abspath(lib)) + '/', ''), line, flush=True)
