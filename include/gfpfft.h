@@ -139,6 +139,19 @@ int gfp_fft_exec_host(gfp_fft_plan *plan, uint64_t *v, int64_t batch, int invers
 int gfp_poly_mul_host(gfp_fft_plan *plan, const uint64_t *f, const uint64_t *g, uint64_t *out,
                       int64_t batch, void *stream);
 
+/* Polynomial product from host coefficient arrays of their own lengths:
+   f is [batch][nf][k], g is [batch][ng][k] (element-major, canonical,
+   1 <= nf, ng <= N), out is [batch][n_out][k] with n_out = min(nf + ng - 1, N):
+   the linear product when nf + ng - 1 <= N (the reference's composition,
+   SURVEY §3.4: zero-pad to N, dft_general both, multiply, dft_inverse),
+   otherwise the first N coefficients of the cyclic product.  Pinned host
+   buffers (cudaHostAlloc / cudaHostRegister) are read by the first
+   transform pass and written by the last one directly (zero-copy: only the
+   nf + ng input and n_out output elements cross PCIe); pageable buffers are
+   staged.  Synchronous. */
+int gfp_poly_mul_host2(gfp_fft_plan *plan, const uint64_t *f, int64_t nf, const uint64_t *g,
+                       int64_t ng, uint64_t *out, int64_t batch, void *stream);
+
 /* Four-step inter-stage twiddle of the sharded transform: x is canonical
    digit-major [batch][k][n]; element (b, i) is multiplied by
    omega^((row0 + b) * i) (omega^-((row0 + b) * i) if inverse), omega the

@@ -50,6 +50,7 @@ SIGNATURES = {
     "gfp_poly_mul": (_int, [_vp, _u64p, _u64p, _u64p, _u64p, _i64, _vp]),
     "gfp_fft_exec_host": (_int, [_vp, _u64p, _i64, _int, _vp]),
     "gfp_poly_mul_host": (_int, [_vp, _u64p, _u64p, _u64p, _i64, _vp]),
+    "gfp_poly_mul_host2": (_int, [_vp, _u64p, _i64, _u64p, _i64, _u64p, _i64, _vp]),
     "gfp_fft_plan_last_launches": (_i64, [_vp]),
     "gfp_fft_twiddle": (_int, [_vp, _u64p, _u64p, _i64, _i64, _i64, _int, _vp]),
     "gfp_probe_imad_wide": (_int, [_i64, _int, _int, ctypes.POINTER(ctypes.c_float),

@@ -82,6 +82,9 @@ static bool fast_bounds(int k, u64 r, FastPlan *out)
     i64 aeps = fp.sp_eps < 0 ? -fp.sp_eps : fp.sp_eps;
     fp.sp_on = aeps < ((i64)1 << 30) && fp.sp_a >= 40 && (aeps << 20) < ((i64)1 << fp.sp_a);
     const int s = fast_split_for(k);
+    // column_quot's shifts: 2s - w and w - 2s must stay below 29
+    if (w + 28 < 2 * s || w > 2 * s + 28)
+        return false;
     const u128 half = (u128)1 << (s - 1);
     const u128 top = (u128)1 << (fp.sp_on ? fp.sp_a : w);
     u128 delta = 2;  // canonical inputs enter through to_balanced (excess <= 1)

@@ -42,8 +42,11 @@ GFP_D u64 column_quot(i64 LL, i64 MID, i64 HH, const RadixConsts &rc, u64 &rem)
     //   w <  2S:  (HH << (2S - w)) + (mid >> (w - S))
     // folded into one branch-free form with sh1 = max(w - 2S, 0),
     // sh2 = max(2S - w, 0) (host-computed)
+    // (fast_bounds keeps q_sh1, q_sh2 <= 28; the masks tell the compiler the
+    // 64-bit shifts are by less than 32, two SHF each)
     const i64 mid = MID + (LL >> S);  // floor((MID 2^S + LL) / 2^S)
-    const i64 t0 = ((HH << rc.q_sh2) + (mid >> (S - rc.q_sh2))) >> rc.q_sh1;
+    const i64 t0 =
+        ((HH << (rc.q_sh2 & 31)) + (mid >> ((S - rc.q_sh2) & 31))) >> (rc.q_sh1 & 31);
     const u64 t = (u64)t0 + rc.bias_t;  // floor(c' / 2^w), in [0, 2^64)
     const u64 clo = (u64)LL + ((u64)MID << S) + ((u64)HH << (2 * S)) + rc.bias_lo;
     const u64 q = t + __umul64hi(t, rc.m_recip);
@@ -57,17 +60,25 @@ GFP_D u64 column_quot(i64 LL, i64 MID, i64 HH, const RadixConsts &rc, u64 &rem)
 // Karatsuba product per digit pair:
 //   MID = sum (xl + xh)(yl + yh) - LL - HH,
 // so a digit product costs three IMAD.WIDE instead of four.
+//
+// negx (bit i set: digit i of x enters negated) lets a caller fold a digit
+// rotation x * r^a, whose wrapped digits change sign (r^k = -1), into the
+// limb split: the negation of a balanced limb pair is again a balanced limb
+// pair, so it costs one IMAD per limb instead of a 64-bit negate.
 template <int KD, bool SPARSE>
 GFP_D void fast_mul_lazy(const i64 (&x)[KD], const i64 (&y)[KD], i64 (&f)[KD],
-                         const RadixConsts &rc)
+                         const RadixConsts &rc, unsigned negx = 0)
 {
     constexpr int S = FastSplit<KD>::S;
     constexpr i64 half = (i64)1 << (S - 1);
     int xl[KD], xh[KD], xs[KD], yl[KD], yh[KD], ys[KD];
 #pragma unroll
     for (int i = 0; i < KD; i++) {
-        xh[i] = (int)((x[i] + half) >> S);
-        xl[i] = (int)(x[i] - ((i64)xh[i] << S));
+        const int h0 = (int)((x[i] + half) >> S);
+        const int l0 = (int)(x[i] - ((i64)h0 << S));
+        const int sg = 1 - (int)((negx >> i) & 1u) * 2;
+        xh[i] = h0 * sg;
+        xl[i] = l0 * sg;
         xs[i] = xl[i] + xh[i];
         yh[i] = (int)((y[i] + half) >> S);
         yl[i] = (int)(y[i] - ((i64)yh[i] << S));

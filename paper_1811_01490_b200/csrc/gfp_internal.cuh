@@ -38,6 +38,25 @@ struct PassArgs {
     int canon;     // canonical output (last pass)
     int in_canon;  // input digits are canonical (convert to balanced on load)
     RadixConsts rc;
+    // element-major I/O (the host entry points; k_pass44 only): when set, the
+    // first pass reads element (b, pos) from in_em + (b n_in + pos) k (zero
+    // for pos >= n_in) instead of `in`, and the last pass writes element
+    // (b, pos < n_out) to out_em + (b n_out + pos) k instead of `out`.  The
+    // pointers may be mapped pinned host memory (zero-copy over PCIe).
+    const u64 *in_em;
+    const u64 *in2_em;
+    int64_t n_in, n_in2;
+    u64 *out_em;
+    int64_t n_out;
+};
+
+// element-major endpoints of one transform (see PassArgs)
+struct EmIO {
+    const u64 *in;
+    const u64 *in2;
+    int64_t n_in, n_in2;
+    u64 *out;
+    int64_t n_out;
 };
 
 // ---------------------------------------------------------------------------
@@ -58,10 +77,16 @@ struct gfp_fft_plan {
 };
 
 // one radix-K Stockham pass (gfp_pass.cuh), instantiated per k in gfp_pass_k*.cu
+// true when the pass kernels of this plan take element-major I/O (EmIO)
+bool em_io_supported(const gfp_fft_plan *p);
+
+// em: element-major first-pass input / last-pass output (nullptr: none);
+// returns GFP_EUNSUPPORTED when em is requested but the kernel for this k
+// cannot do it (the caller then stages through digit-major buffers)
 template <int KD>
 int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2, u64 *out2,
                 const u64 *pre, int64_t batch, int64_t Ns, int inverse, int scale, int canon,
-                int in_canon, cudaStream_t st);
+                int in_canon, const EmIO *em, cudaStream_t st);
 
 #define DISPATCH_K(k, CALL)                                                                     \
     switch (k) {                                                                                \

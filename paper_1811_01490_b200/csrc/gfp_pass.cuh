@@ -10,6 +10,7 @@
 #pragma once
 #include "gfp_internal.cuh"
 #include "gfp_fast.cuh"
+#include "gfp_pass44.cuh"
 
 template <int KD>
 GFP_D i64 rot_lane(i64 val, int t, int d, bool inverse)
@@ -247,7 +248,7 @@ static size_t pass_smem(int G)
 template <int KD>
 int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
                        u64 *out2, const u64 *pre, int64_t batch, int64_t Ns, int inverse,
-                       int scale, int canon, int in_canon, cudaStream_t st)
+                       int scale, int canon, int in_canon, const EmIO *em, cudaStream_t st)
 {
     int G;
     int threads = pass_threads(KD, p->M, &G);
@@ -280,6 +281,25 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
     A.in2 = in2;
     A.out2 = out2;
     A.batch = batch;
+    A.in_em = A.in2_em = nullptr;
+    A.out_em = nullptr;
+    A.n_in = A.n_in2 = A.n_out = 0;
+    if (em) {
+        if (Ns == 1 && em->in) {
+            A.in_em = em->in;
+            A.in2_em = em->in2;
+            A.n_in = em->n_in;
+            A.n_in2 = em->n_in2;
+        }
+        if (canon && em->out) {
+            A.out_em = em->out;
+            A.n_out = em->n_out;
+        }
+    }
+    if (launch_pass44<KD>(A, p->M, in2 ? 2 * batch : batch, st))
+        return cuda_status();
+    if (A.in_em || A.out_em)
+        return GFP_EUNSUPPORTED;
     dim3 grid((unsigned)((p->M + G - 1) / G), (unsigned)(in2 ? 2 * batch : batch));
     if (p->rc.sp_on) {
         k_pass<KD, true><<<grid, threads, smem, st>>>(A);

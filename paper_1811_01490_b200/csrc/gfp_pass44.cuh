@@ -1,0 +1,364 @@
+// gfp_pass44.cuh -- radix-16 Stockham pass for k = 8 (K = 2k = 16), thread
+// per element throughout (no warp shuffles).
+//
+// Same pass as k_pass (gfp_pass.cuh): group j of M = N/K groups reads
+// x[j + t M] (t < K), multiplies element t by omega^E,
+// E = t (j mod Ns) (M / Ns), and writes the K-point DFT at root rho = r (or
+// 1/r) to (j / Ns) Ns K + (j mod Ns) + u Ns.  The reference computes the
+// same transform with dft_general (fft.py:298-360): base-case blocks of
+// dft2 / r^t shifts (fft.py:114-193) and level twiddles split as
+// r^a * omega^b (_twiddle_level_cheap, fft.py:84-103).
+//
+// Mapping (CTA = 4 warps x 32 lanes, 32 consecutive groups, lane = group):
+//   phase A   warp w loads elements t = w + 4 t2 (t2 < 4) of its lane's
+//             group.  r^a is folded into the digit addressing of the load
+//             (digit d comes from row (d - a) mod k) and the wrapped digits'
+//             sign into the multiply's limb split; omega^b is one general
+//             multiply (fast_mul_lazy) by the table entry.
+//             Each finished element is parked in the thread's own smem slot
+//             (keeping four in registers across the multiplies halves occupancy).
+//   stage 1   4-point DFT over t2 at root rho^4 (a rotation by k/2 digits):
+//             pure adds with compile-time digit renaming, in registers.
+//   exchange  outputs Y[w][u0] through shared memory (one 80 B slot each).
+//   stage 2   warp w = u0 gathers Y[t1][u0], applies rho^(t1 u0) as a
+//             compile-time rotation (warp-uniform switch on u0) whose sign
+//             flips fold into the adds, and runs the 4-point DFT over t1:
+//             X[u0 + 4 u1].  One balanced normalisation per element, the
+//             canonical form on the last pass, coalesced digit-row stores.
+// K = 16 = 4 x 4 needs 4 lazy radix-2 stages without normalisation; the
+// launcher only selects this kernel when the host bound check allows it
+// (RadixConsts::stages_per_norm >= 4).
+#pragma once
+#include "gfp_internal.cuh"
+#include "gfp_fast.cuh"
+
+#ifndef P44_MINB
+#define P44_MINB 5  // CTAs per SM the NW = 4 variant is register-bounded for
+#endif
+
+namespace p44 {
+
+// y = x * r^S for a compile-time S in [0, 2k): digit renaming, wrapped
+// digits negated (r^k = -1)
+template <int KD, int S>
+GFP_D void rot_c(const i64 (&x)[KD], i64 (&y)[KD])
+{
+    constexpr int s = S % KD;
+    constexpr bool negall = ((S / KD) & 1) != 0;
+#pragma unroll
+    for (int d = 0; d < KD; d++) {
+        const int src = (d - s + KD) % KD;
+        const bool wrap = d < s;
+        y[d] = (wrap != negall) ? -x[src] : x[src];
+    }
+}
+
+// exponent of rho^e as a power of r: rho = r (forward) or 1/r = r^(2k-1)
+template <int KD, bool INV>
+__host__ __device__ constexpr int rexp(int e)
+{
+    return INV ? (2 * KD - (e % (2 * KD))) % (2 * KD) : e % (2 * KD);
+}
+
+// in-place 4-point DFT at root w = rho^(K/4) (w^2 = -1):
+//   Z0 = (x0 + x2) + (x1 + x3)   Z2 = (x0 + x2) - (x1 + x3)
+//   Z1 = (x0 - x2) + w(x1 - x3)  Z3 = (x0 - x2) - w(x1 - x3)
+// x1 and x3 may first be multiplied by rho^(T1) and rho^(3 T1), x2 by
+// rho^(2 T1) (stage 2's inter-stage twiddle, T1 = u0), as compile-time
+// rotations whose sign flips the compiler folds into the adds.
+template <int KD, bool INV, int TW>
+GFP_D void dft4(i64 (&x0)[KD], i64 (&x1)[KD], i64 (&x2)[KD], i64 (&x3)[KD])
+{
+    i64 a1[KD], a2[KD], a3[KD];
+    rot_c<KD, rexp<KD, INV>(TW)>(x1, a1);
+    rot_c<KD, rexp<KD, INV>(2 * TW)>(x2, a2);
+    rot_c<KD, rexp<KD, INV>(3 * TW)>(x3, a3);
+    i64 s0[KD], d0[KD], s1[KD], t[KD], d1[KD];
+#pragma unroll
+    for (int d = 0; d < KD; d++) {
+        s0[d] = x0[d] + a2[d];
+        d0[d] = x0[d] - a2[d];
+        s1[d] = a1[d] + a3[d];
+        t[d] = a1[d] - a3[d];
+    }
+    rot_c<KD, rexp<KD, INV>(KD / 2)>(t, d1);  // w = rho^(K/4) = rho^(k/2)
+#pragma unroll
+    for (int d = 0; d < KD; d++) {
+        x0[d] = s0[d] + s1[d];
+        x2[d] = s0[d] - s1[d];
+        x1[d] = d0[d] + d1[d];
+        x3[d] = d0[d] - d1[d];
+    }
+}
+
+// one balanced normalisation of a lazy element: digit quotients move one
+// digit up, the top one wraps negated into digit 0 (r^k = -1)
+template <int KD, bool SPARSE>
+GFP_D void normalize_el(i64 (&v)[KD], const RadixConsts &rc)
+{
+    int q[KD];
+    i64 rem[KD];
+#pragma unroll
+    for (int d = 0; d < KD; d++)
+        q[d] = norm_bal<SPARSE>(v[d], rc, rem[d]);
+    v[0] = rem[0] - q[KD - 1];
+#pragma unroll
+    for (int d = 1; d < KD; d++)
+        v[d] = rem[d] + q[d - 1];
+}
+
+}  // namespace p44
+
+template <int KD, bool SPARSE, bool INV, int NW>
+__global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1) k_pass44(PassArgs A)
+{
+    static_assert(KD == 8, "radix 4 x 4 pass is for K = 16");
+    constexpr int K = 2 * KD;
+    constexpr int SLOT = KD + 2;  // 80 B element slot: conflict-free 128-bit smem access
+    __shared__ __align__(16) i64 sm[K * 32 * SLOT];
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;  // t1 in stage 1, u0 in stage 2 (warp-uniform)
+
+    int64_t bidx = blockIdx.y;
+    const u64 *in_base = A.in;
+    u64 *out_base = A.out;
+    const u64 *em_in = A.in_em;
+    int64_t n_in = A.n_in;
+    if (bidx >= A.batch) {
+        bidx -= A.batch;
+        in_base = A.in2;
+        out_base = A.out2;
+        em_in = A.in2_em;
+        n_in = A.n_in2;
+    }
+    if (em_in)
+        em_in += bidx * n_in * KD;
+    u64 *em_out = A.out_em ? A.out_em + bidx * A.n_out * KD : nullptr;
+    const int lN = A.lN, lM = A.lM, lNs = A.lNs;
+    const int64_t N = (int64_t)1 << lN, M = (int64_t)1 << lM;
+    const int64_t nsmask = ((int64_t)1 << lNs) - 1;
+    const u64 *in = in_base + bidx * A.batch_stride;
+    u64 *out = out_base + bidx * A.batch_stride;
+    const u64 *pre = A.pre ? A.pre + bidx * A.batch_stride : nullptr;
+    const RadixConsts rc = A.rc;
+    const int64_t j = ((int64_t)blockIdx.x << 5) + lane;
+    const bool active = j < M;
+
+    // ---- phase A: load + twiddle elements t = w + NW i (16 / NW per thread)
+    i64 e[4][KD];
+#pragma unroll 1
+    for (int i = 0; i < 16 / NW; i++) {
+        const int t = w + NW * i;
+        i64 f[KD], x[KD];
+        int64_t b = 0;
+        unsigned negx = 0;
+        const int64_t pos = j + ((int64_t)t << lM);
+        if (active) {
+            // E = t (j mod Ns) (M / Ns) < N; omega^E = r^a omega^b
+            int64_t E = ((int64_t)t * (j & nsmask)) << (lM - lNs);
+            if (A.neg_exp && E)
+                E = N - E;
+            int a = (int)(E >> lM);
+            b = E & (M - 1);
+            if (A.root_inv && a)
+                a = 2 * KD - a;
+            // x * r^a: digit d comes from row (d - a) mod k, negated when it
+            // wrapped (d < a mod k) xor a >= k
+            const int as = a & (KD - 1);
+            negx = ((1u << as) - 1u) ^ (a >= KD ? ((1u << KD) - 1u) : 0u);
+            if (em_in) {  // first pass (a = 0): element-major, zero-padded past n_in
+                if (pos < n_in) {
+                    const ulonglong2 *ep = reinterpret_cast<const ulonglong2 *>(em_in + pos * KD);
+#pragma unroll
+                    for (int d = 0; d < KD; d += 2) {
+                        const ulonglong2 v = ep[d / 2];
+                        x[d] = (i64)v.x;
+                        x[d + 1] = (i64)v.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int d = 0; d < KD; d++)
+                        x[d] = 0;
+                }
+            } else {
+                const u64 *src = in + pos;
+#pragma unroll
+                for (int d = 0; d < KD; d++)
+                    x[d] = (i64)__ldg(src + ((int64_t)((d - as) & (KD - 1)) << lN));
+            }
+            if (A.in_canon)  // pass 0 only, where a = 0
+                to_balanced<KD>(x, rc.r);
+            if (pre) {  // pass 0 only (a = b = 0): pointwise product
+                i64 y[KD];
+#pragma unroll
+                for (int d = 0; d < KD; d++)
+                    y[d] = (i64)__ldg(pre + ((int64_t)d << lN) + pos);
+                fast_mul_lazy<KD, SPARSE>(x, y, x, rc);
+            }
+        }
+        // the multiply is warp-uniform: lanes whose twiddle is a pure power
+        // of r (b = 0) multiply by table[0] = 1 instead of diverging
+        if (__any_sync(FULL_MASK, active && (b || A.scale))) {
+            if (active) {
+                i64 y[KD];
+                const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(A.table + b * KD);
+#pragma unroll
+                for (int d = 0; d < KD; d += 2) {
+                    const ulonglong2 v = __ldg(tp + d / 2);
+                    y[d] = (i64)v.x;
+                    y[d + 1] = (i64)v.y;
+                }
+                fast_mul_lazy<KD, SPARSE>(x, y, f, rc, negx);
+            }
+        } else if (active) {
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                f[d] = ((negx >> d) & 1u) ? -x[d] : x[d];
+        }
+        if (!active) {
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                f[d] = 0;
+        }
+        // park element t in slot t: holding four elements in registers
+        // across the multiplies would cost occupancy
+        i64 *slot = sm + (t * 32 + lane) * SLOT;
+#pragma unroll
+        for (int d = 0; d < KD; d += 2)
+            *reinterpret_cast<longlong2 *>(slot + d) = make_longlong2(f[d], f[d + 1]);
+    }
+
+    // ---- stage 1 (warps w < 4, t1 = w): 4-point DFT over t2 (root rho^4) of
+    // slots t1 + 4 t2, outputs u0 = 0..3 back into slots t1 + 4 u0 (the same
+    // slots: no other thread touches them).  With NW = 4 the thread reads
+    // its own phase-A slots and needs no barrier.
+    if (NW > 4)
+        __syncthreads();
+    if (w < 4) {
+#pragma unroll
+    for (int t2 = 0; t2 < 4; t2++) {
+        const i64 *slot = sm + ((t2 * 4 + w) * 32 + lane) * SLOT;
+#pragma unroll
+        for (int d = 0; d < KD; d += 2) {
+            const longlong2 v = *reinterpret_cast<const longlong2 *>(slot + d);
+            e[t2][d] = v.x;
+            e[t2][d + 1] = v.y;
+        }
+    }
+    p44::dft4<KD, INV, 0>(e[0], e[1], e[2], e[3]);
+#pragma unroll
+    for (int u0 = 0; u0 < 4; u0++) {
+        i64 *slot = sm + ((u0 * 4 + w) * 32 + lane) * SLOT;
+#pragma unroll
+        for (int d = 0; d < KD; d += 2)
+            *reinterpret_cast<longlong2 *>(slot + d) = make_longlong2(e[u0][d], e[u0][d + 1]);
+    }
+    }
+    __syncthreads();
+    if (w >= 4)
+        return;
+
+    // ---- stage 2: u0 = w; gather Y[t1][u0], twiddle rho^(t1 u0), DFT over t1
+#pragma unroll
+    for (int t1 = 0; t1 < 4; t1++) {
+        const i64 *slot = sm + ((w * 4 + t1) * 32 + lane) * SLOT;
+#pragma unroll
+        for (int d = 0; d < KD; d += 2) {
+            const longlong2 v = *reinterpret_cast<const longlong2 *>(slot + d);
+            e[t1][d] = v.x;
+            e[t1][d + 1] = v.y;
+        }
+    }
+    switch (w) {
+    case 0: p44::dft4<KD, INV, 0>(e[0], e[1], e[2], e[3]); break;
+    case 1: p44::dft4<KD, INV, 1>(e[0], e[1], e[2], e[3]); break;
+    case 2: p44::dft4<KD, INV, 2>(e[0], e[1], e[2], e[3]); break;
+    default: p44::dft4<KD, INV, 3>(e[0], e[1], e[2], e[3]); break;
+    }
+    if (!active)
+        return;
+    // X[u0 + 4 u1] = e[u1] -> (j / Ns) Ns K + (j mod Ns) + u Ns
+    const int64_t base = ((j >> lNs) << (lNs + 4)) + (j & nsmask);
+#pragma unroll
+    for (int u1 = 0; u1 < 4; u1++) {
+        p44::normalize_el<KD, SPARSE>(e[u1], rc);
+        const int64_t pos = base + ((int64_t)(w + 4 * u1) << lNs);
+        if (A.canon) {
+            u64 c[KD];
+            lazy_to_canonical(e[u1], c, KD, rc);
+            if (em_out) {  // last pass: element-major, the first n_out elements
+                if (pos < A.n_out) {
+                    ulonglong2 *ep = reinterpret_cast<ulonglong2 *>(em_out + pos * KD);
+#pragma unroll
+                    for (int d = 0; d < KD; d += 2)
+                        ep[d / 2] = make_ulonglong2(c[d], c[d + 1]);
+                }
+            } else {
+#pragma unroll
+                for (int d = 0; d < KD; d++)
+                    out[((int64_t)d << lN) + pos] = c[d];
+            }
+        } else {
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                out[((int64_t)d << lN) + pos] = (u64)e[u1][d];
+        }
+    }
+}
+
+// k_pass44 serves k = 8 when 4 lazy radix-2 stages fit the digit bounds
+static inline bool pass44_enabled(int k, const RadixConsts &rc)
+{
+    static int disabled = -1;
+    if (disabled < 0) {
+        const char *e = getenv("GFP_PASS44");  // experiment hook: 0 = old kernel
+        disabled = (e && e[0] == '0') ? 1 : 0;
+    }
+    return k == 8 && !disabled && rc.stages_per_norm >= 4;
+}
+
+// launcher: returns 1 when it handled the pass
+template <int KD>
+static int launch_pass44(const PassArgs &A, int64_t M, int64_t nsets, cudaStream_t st)
+{
+    if constexpr (KD != 8) {
+        return 0;
+    } else {
+        if (!pass44_enabled(KD, A.rc))
+            return 0;
+        const int64_t ctas = ((M + 31) / 32) * nsets;
+        dim3 grid((unsigned)((M + 31) / 32), (unsigned)nsets);
+        // elements per thread in phase A: 4 when the grid fills the GPU,
+        // fewer (more warps per CTA) for small transforms (C1, C2)
+        static int nw_env = -1;
+        if (nw_env < 0) {
+            const char *e = getenv("GFP_PASS44_NW");  // experiment hook
+            nw_env = e ? atoi(e) : 0;
+        }
+        int nw = ctas >= 4 * (int64_t)num_sms() ? 4 : ctas >= (int64_t)num_sms() ? 8 : 16;
+        if (nw_env == 4 || nw_env == 8 || nw_env == 16)
+            nw = nw_env;
+        const bool inv = A.rot_inv != 0;
+#define P44_LAUNCH(SP, IV)                                                                    \
+    switch (nw) {                                                                             \
+    case 4: k_pass44<KD, SP, IV, 4><<<grid, 128, 0, st>>>(A); break;                          \
+    case 8: k_pass44<KD, SP, IV, 8><<<grid, 256, 0, st>>>(A); break;                          \
+    default: k_pass44<KD, SP, IV, 16><<<grid, 512, 0, st>>>(A); break;                        \
+    }
+        if (A.rc.sp_on) {
+            if (inv) {
+                P44_LAUNCH(true, true)
+            } else {
+                P44_LAUNCH(true, false)
+            }
+        } else {
+            if (inv) {
+                P44_LAUNCH(false, true)
+            } else {
+                P44_LAUNCH(false, false)
+            }
+        }
+#undef P44_LAUNCH
+        return 1;
+    }
+}

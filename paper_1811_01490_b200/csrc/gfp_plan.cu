@@ -159,7 +159,7 @@ __global__ void k_twiddle_rows(const u64 *__restrict__ x, u64 *__restrict__ out,
 // pass (single set only).
 static int run_transform2(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, const u64 *in_b,
                           u64 *out_b, u64 *work_b, const u64 *pre, int64_t batch, int inverse,
-                          int in_canon, int out_canon, cudaStream_t st)
+                          int in_canon, int out_canon, cudaStream_t st, const EmIO *em = nullptr)
 {
     // ping-pong so that the last pass lands in `out`; inputs are never written
     int e = p->e;
@@ -182,7 +182,7 @@ static int run_transform2(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, c
         int rcode;
         DISPATCH_FAST_K(p->k, (rcode = launch_pass<KD>(p, src, dst, src_b, dst_b, pre_p, batch,
                                                        Ns, inverse, scale, last && out_canon,
-                                                       pass == 0 && in_canon, st)));
+                                                       pass == 0 && in_canon, em, st)));
         if (rcode)
             return rcode;
         p->last_launches++;
@@ -190,6 +190,8 @@ static int run_transform2(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, c
         src_b = dst_b;
         Ns *= p->K;
     }
+    if (em && em->out && out_canon)
+        return cuda_status();  // the last pass wrote the element-major output
     if (src != out)
         cudaMemcpyAsync(out, src, sizeof(u64) * (size_t)p->k * p->N * batch,
                         cudaMemcpyDeviceToDevice, st);
@@ -201,10 +203,10 @@ static int run_transform2(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, c
 
 static int run_transform(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, const u64 *pre,
                          int64_t batch, int inverse, int in_canon, int out_canon,
-                         cudaStream_t st)
+                         cudaStream_t st, const EmIO *em = nullptr)
 {
     return run_transform2(p, in, out, work, nullptr, nullptr, nullptr, pre, batch, inverse,
-                          in_canon, out_canon, st);
+                          in_canon, out_canon, st, em);
 }
 
 extern "C" {
@@ -436,27 +438,109 @@ static int ensure_host_scratch(gfp_fft_plan *p, int64_t words)
     return GFP_OK;
 }
 
-int gfp_fft_exec_host(gfp_fft_plan *p, uint64_t *v, int64_t batch, int inverse, void *stream)
+// Device alias of a host pointer: pinned (cudaHostAlloc / cudaHostRegister)
+// memory is mapped into the device address space, so the first and last
+// transform passes read and write it directly over PCIe (no staging copy,
+// no transpose kernel).  Pageable memory returns nullptr: the caller stages.
+static u64 *mapped_alias(const void *h)
 {
-    if (!p || !v || batch < 1)
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (at.type == cudaMemoryTypeHost && at.devicePointer)
+        return (u64 *)at.devicePointer;
+    return nullptr;
+}
+
+// the staged route for kernels without element-major I/O (k != 8): zero-pad
+// into digit-major device vectors, transform, transpose back
+static int poly_mul_host_staged(gfp_fft_plan *p, const u64 *f, int64_t nf, const u64 *g,
+                                int64_t ng, u64 *out, int64_t n_out, int64_t batch,
+                                cudaStream_t st)
+{
+    const int k = p->k;
+    const int64_t N = p->N, vw = (int64_t)k * N * batch;
+    int err = ensure_host_scratch(p, 7 * vw);
+    if (err)
+        return err;
+    u64 *hf = p->h_dev, *hg = hf + vw, *df = hg + vw, *dg = df + vw, *w = dg + vw;
+    cudaMemsetAsync(hf, 0, sizeof(u64) * 2 * vw, st);
+    for (int64_t i = 0; i < batch; i++) {
+        cudaMemcpyAsync(hf + i * k * N, f + i * k * nf, sizeof(u64) * k * nf,
+                        cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(hg + i * k * N, g + i * k * ng, sizeof(u64) * k * ng,
+                        cudaMemcpyHostToDevice, st);
+        gfp_to_digit_major(hf + i * k * N, df + i * k * N, N, k, st);
+        gfp_to_digit_major(hg + i * k * N, dg + i * k * N, N, k, st);
+    }
+    err = gfp_poly_mul(p, df, dg, df, w, batch, st);
+    if (err)
+        return err;
+    for (int64_t i = 0; i < batch; i++) {
+        gfp_to_element_major(df + i * k * N, hf + i * k * N, N, k, st);
+        cudaMemcpyAsync(out + i * k * n_out, hf + i * k * N, sizeof(u64) * k * n_out,
+                        cudaMemcpyDeviceToHost, st);
+    }
+    p->last_launches += 3 * batch;
+    return GFP_OK;
+}
+
+int gfp_poly_mul_host2(gfp_fft_plan *p, const uint64_t *f, int64_t nf, const uint64_t *g,
+                       int64_t ng, uint64_t *out, int64_t batch, void *stream)
+{
+    if (!p || !f || !g || !out || batch < 1 || nf < 1 || ng < 1 || nf > p->N || ng > p->N)
         return GFP_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
-    int64_t vw = (int64_t)p->k * p->N * batch;
-    int err = ensure_host_scratch(p, 3 * vw);
-    if (err)
-        return err;
-    u64 *a = p->h_dev, *b = a + vw, *w = b + vw;
-    cudaMemcpyAsync(a, v, sizeof(u64) * vw, cudaMemcpyHostToDevice, st);
+    const int k = p->k;
+    const int64_t N = p->N, vw = (int64_t)k * N * batch;
+    const int64_t n_out = nf + ng - 1 < N ? nf + ng - 1 : N;
     p->last_launches = 0;
-    for (int64_t i = 0; i < batch; i++)
-        gfp_to_digit_major(a + i * p->k * p->N, b + i * p->k * p->N, p->N, p->k, st);
-    err = run_transform(p, b, b, w, nullptr, batch, inverse ? 1 : 0, 1, 1, st);
+    if (!em_io_supported(p)) {
+        int err = poly_mul_host_staged(p, f, nf, g, ng, out, n_out, batch, st);
+        if (err)
+            return err;
+        if (cudaStreamSynchronize(st) != cudaSuccess)
+            return GFP_ECUDA;
+        return cuda_status();
+    }
+    const u64 *mf = mapped_alias(f), *mg = mapped_alias(g);
+    u64 *mo = mapped_alias(out);
+    // device workspace: the two spectra, two ping-pong buffers, and staging
+    // for whichever operand is not mapped
+    const int64_t stage_words = (mf ? 0 : k * nf * batch) + (mg ? 0 : k * ng * batch) +
+                                (mo ? 0 : k * n_out * batch);
+    int err = ensure_host_scratch(p, 4 * vw + stage_words);
     if (err)
         return err;
-    for (int64_t i = 0; i < batch; i++)
-        gfp_to_element_major(b + i * p->k * p->N, a + i * p->k * p->N, p->N, p->k, st);
-    p->last_launches += 2 * batch;
-    cudaMemcpyAsync(v, a, sizeof(u64) * vw, cudaMemcpyDeviceToHost, st);
+    u64 *F = p->h_dev, *G = F + vw, *s1 = G + vw, *s2 = s1 + vw, *stg = s2 + vw;
+    if (!mf) {
+        cudaMemcpyAsync(stg, f, sizeof(u64) * k * nf * batch, cudaMemcpyHostToDevice, st);
+        mf = stg;
+        stg += k * nf * batch;
+    }
+    if (!mg) {
+        cudaMemcpyAsync(stg, g, sizeof(u64) * k * ng * batch, cudaMemcpyHostToDevice, st);
+        mg = stg;
+        stg += k * ng * batch;
+    }
+    u64 *dout = mo ? mo : stg;
+    // forward transforms of both operands in the same launches; pass 0 reads
+    // the element-major operands (zero past nf / ng); spectra stay lazy
+    EmIO e1 = {mf, mg, nf, ng, nullptr, 0};
+    err = run_transform2(p, F, F, s1, G, G, s2, nullptr, batch, 0, 1, 0, st, &e1);
+    if (!err) {
+        // inverse of F .* G (pointwise product fused into pass 0, N^-1 into
+        // the last pass), which writes the first n_out elements element-major
+        EmIO e2 = {nullptr, nullptr, 0, 0, dout, n_out};
+        err = run_transform(p, F, F, s1, G, batch, 1, 0, 1, st, &e2);
+    }
+    if (!err && !mo) {
+        cudaMemcpyAsync(out, dout, sizeof(u64) * k * n_out * batch, cudaMemcpyDeviceToHost, st);
+    }
+    if (err)
+        return err;
     if (cudaStreamSynchronize(st) != cudaSuccess)
         return GFP_ECUDA;
     return cuda_status();
@@ -465,27 +549,53 @@ int gfp_fft_exec_host(gfp_fft_plan *p, uint64_t *v, int64_t batch, int inverse, 
 int gfp_poly_mul_host(gfp_fft_plan *p, const uint64_t *f, const uint64_t *g, uint64_t *out,
                       int64_t batch, void *stream)
 {
-    if (!p || !f || !g || !out || batch < 1)
+    if (!p)
+        return GFP_EINVAL;
+    return gfp_poly_mul_host2(p, f, p->N, g, p->N, out, batch, stream);
+}
+
+int gfp_fft_exec_host(gfp_fft_plan *p, uint64_t *v, int64_t batch, int inverse, void *stream)
+{
+    if (!p || !v || batch < 1)
         return GFP_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
-    int64_t vw = (int64_t)p->k * p->N * batch;
-    int err = ensure_host_scratch(p, 7 * vw);
+    const int k = p->k;
+    const int64_t N = p->N, vw = (int64_t)k * N * batch;
+    p->last_launches = 0;
+    u64 *mv = em_io_supported(p) ? mapped_alias(v) : nullptr;
+    // a single-pass transform would read and write v in the same launch:
+    // stage its output
+    const bool stage_out = !mv || p->e == 1;
+    int err = ensure_host_scratch(p, 3 * vw + (mv ? 0 : vw));
     if (err)
         return err;
-    u64 *hf = p->h_dev, *hg = hf + vw, *df = hg + vw, *dg = df + vw, *w = dg + vw;
-    cudaMemcpyAsync(hf, f, sizeof(u64) * vw, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(hg, g, sizeof(u64) * vw, cudaMemcpyHostToDevice, st);
-    for (int64_t i = 0; i < batch; i++) {
-        gfp_to_digit_major(hf + i * p->k * p->N, df + i * p->k * p->N, p->N, p->k, st);
-        gfp_to_digit_major(hg + i * p->k * p->N, dg + i * p->k * p->N, p->N, p->k, st);
+    u64 *a = p->h_dev, *b = a + vw, *w = b + vw;
+    const u64 *src = mv;
+    if (!mv) {
+        u64 *stg = w + vw;
+        cudaMemcpyAsync(stg, v, sizeof(u64) * vw, cudaMemcpyHostToDevice, st);
+        src = stg;
     }
-    err = gfp_poly_mul(p, df, dg, df, w, batch, st);
-    if (err)
-        return err;
-    for (int64_t i = 0; i < batch; i++)
-        gfp_to_element_major(df + i * p->k * p->N, hf + i * p->k * p->N, p->N, p->k, st);
-    p->last_launches += 3 * batch;
-    cudaMemcpyAsync(out, hf, sizeof(u64) * vw, cudaMemcpyDeviceToHost, st);
+    if (!em_io_supported(p)) {
+        // no element-major kernel for this k: transpose around the transform
+        cudaMemcpyAsync(a, src, sizeof(u64) * vw, cudaMemcpyDeviceToDevice, st);
+        for (int64_t i = 0; i < batch; i++)
+            gfp_to_digit_major(a + i * k * N, b + i * k * N, N, k, st);
+        err = run_transform(p, b, b, w, nullptr, batch, inverse ? 1 : 0, 1, 1, st);
+        if (err)
+            return err;
+        for (int64_t i = 0; i < batch; i++)
+            gfp_to_element_major(b + i * k * N, a + i * k * N, N, k, st);
+        p->last_launches += 2 * batch;
+        cudaMemcpyAsync(v, a, sizeof(u64) * vw, cudaMemcpyDeviceToHost, st);
+    } else {
+        EmIO em = {src, nullptr, N, 0, stage_out ? a : mv, N};
+        err = run_transform(p, b, b, w, nullptr, batch, inverse ? 1 : 0, 1, 1, st, &em);
+        if (err)
+            return err;
+        if (stage_out)
+            cudaMemcpyAsync(v, a, sizeof(u64) * vw, cudaMemcpyDeviceToHost, st);
+    }
     if (cudaStreamSynchronize(st) != cudaSuccess)
         return GFP_ECUDA;
     return cuda_status();

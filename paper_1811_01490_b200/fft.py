@@ -202,9 +202,17 @@ def last_launches(plan):
 # ---------------------------------------------------------------------------
 # host-buffer entry points (the e2e path: H2D, transform, D2H in one C call)
 
-def fft_host(v, plan, inverse=False):
-    """Element-major host array [N, k] or [B, N, k] (uint64) -> new array."""
-    a = np.ascontiguousarray(np.asarray(v, dtype=np.uint64)).copy()
+def fft_host(v, plan, inverse=False, inplace=False):
+    """Element-major host array [N, k] or [B, N, k] (uint64) -> new array, or
+    v itself transformed in place (inplace=True: v must be a C-contiguous
+    uint64 array; pinned memory is then read and written by the kernels
+    directly)."""
+    if inplace:
+        if not (isinstance(v, np.ndarray) and v.dtype == np.uint64 and v.flags.c_contiguous):
+            raise ValueError("inplace needs a C-contiguous uint64 array")
+        a = v
+    else:
+        a = np.ascontiguousarray(np.asarray(v, dtype=np.uint64)).copy()
     B = a.size // (plan.N * plan.params.k)
     _lib.check(_lib.load().gfp_fft_exec_host(plan.handle, ctypes.c_void_p(a.ctypes.data), B,
                                             1 if inverse else 0, _stream()),
@@ -213,15 +221,28 @@ def fft_host(v, plan, inverse=False):
 
 
 def poly_mul_host(f, g, plan):
+    """Product of host coefficient arrays [n, k] (or [B, n, k]) with n <= N:
+    [min(nf + ng - 1, N), k] -- the linear product when it fits in N, else
+    the cyclic one (N-length inputs give the length-N cyclic product)."""
     f = np.ascontiguousarray(np.asarray(f, dtype=np.uint64))
     g = np.ascontiguousarray(np.asarray(g, dtype=np.uint64))
-    out = np.empty_like(f)
-    B = f.size // (plan.N * plan.params.k)
-    _lib.check(_lib.load().gfp_poly_mul_host(plan.handle, ctypes.c_void_p(f.ctypes.data),
-                                            ctypes.c_void_p(g.ctypes.data),
-                                            ctypes.c_void_p(out.ctypes.data), B, _stream()),
-               "gfp_poly_mul_host")
-    return out
+    k = plan.params.k
+    if f.ndim == 2:
+        f, g, squeeze = f[None], g[None], True
+    else:
+        squeeze = False
+    B, nf, ng = f.shape[0], f.shape[1], g.shape[1]
+    if g.shape[0] != B or f.shape[2] != k or g.shape[2] != k:
+        raise ValueError("operand shapes must be [n, k] (or [B, n, k]) with matching B")
+    if not (1 <= nf <= plan.N and 1 <= ng <= plan.N):
+        raise ValueError("polynomial lengths must be in [1, N]")
+    n_out = min(nf + ng - 1, plan.N)
+    out = np.empty((B, n_out, k), dtype=np.uint64)
+    _lib.check(_lib.load().gfp_poly_mul_host2(plan.handle, ctypes.c_void_p(f.ctypes.data), nf,
+                                             ctypes.c_void_p(g.ctypes.data), ng,
+                                             ctypes.c_void_p(out.ctypes.data), B, _stream()),
+               "gfp_poly_mul_host2")
+    return out[0] if squeeze else out
 
 
 # ---------------------------------------------------------------------------

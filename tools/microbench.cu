@@ -97,6 +97,38 @@ __global__ void k_add64(int64_t iters, int b0, int64_t *out) {
     if (s == 0x1234567) out[threadIdx.x] = s;
 }
 
+// pure IMAD.WIDE issue rate: each wide product's halves become the next
+// operands (no ALU work; ptxas emits one IMAD.WIDE per product)
+__global__ void k_wide_rz(int64_t iters, int b0, int64_t *out) {
+    int a[NCH], b[NCH];
+    for (int c = 0; c < NCH; c++) { a[c] = threadIdx.x + c; b[c] = b0 + c; }
+    for (int64_t i = 0; i < iters; i++)
+#pragma unroll
+        for (int c = 0; c < NCH; c++) {
+            int64_t d;
+            asm volatile("mul.wide.s32 %0, %1, %2;" : "=l"(d) : "r"(a[c]), "r"(b[c]));
+            a[c] = (int)(d >> 32);
+            b[c] = (int)d;
+        }
+    int s = 0; for (int c = 0; c < NCH; c++) s ^= a[c] ^ b[c];
+    if (s == 0x1234567) out[threadIdx.x] = s;
+}
+
+// product accumulated into 64 bits as ptxas compiles it on sm_100a:
+// IMAD.WIDE with RZ plus a 64-bit add (IADD3 + IADD3.X / IMAD.X)
+__global__ void k_wide_acc(int64_t iters, int b0, int64_t *out) {
+    int64_t acc[NCH]; int a[NCH];
+    for (int c = 0; c < NCH; c++) { acc[c] = threadIdx.x + c; a[c] = threadIdx.x * 3 + c; }
+    for (int64_t i = 0; i < iters; i++)
+#pragma unroll
+        for (int c = 0; c < NCH; c++) {
+            asm volatile("mad.wide.s32 %0, %1, %2, %0;" : "+l"(acc[c]) : "r"(a[c]), "r"(b0 + c));
+            a[c] = (int)(acc[c] >> 32);
+        }
+    int64_t s = 0; for (int c = 0; c < NCH; c++) s ^= acc[c];
+    if (s == 0x1234567) out[threadIdx.x] = s;
+}
+
 template <typename F>
 double run(F kern, const char *name, int sms, double mhz) {
     int64_t *out; cudaMalloc(&out, 1 << 20);
@@ -118,6 +150,8 @@ double run(F kern, const char *name, int sms, double mhz) {
 int main(int argc, char **argv) {
     double mhz = argc > 1 ? atof(argv[1]) : 1965.0;
     int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    run(k_wide_rz, "IMAD.WIDE only", sms, mhz);
+    run(k_wide_acc, "IMAD.WIDE+64b add", sms, mhz);
     run(k_madwide_s32, "mad.wide.s32 chain", sms, mhz);
     run(k_madwide_u32, "mad.wide.u32 chain", sms, mhz);
     run(k_madwide_u32_ind, "mad.wide.u32 ind+lop", sms, mhz);
