@@ -451,8 +451,8 @@ def run_ours(args, ws, rank, local):
                      "traffic": traffic,
                      "algorithmic": "%d general multiplies x 3k^2 = %d IMAD.WIDE per step (executed; 4k^2 schoolbook limb products)"
                                     % (mults, imad),
-                     "peak_source": "measured live: gfp_probe_imad_wide (8 independent "
-                                    "mad.wide.s32 chains/thread, best of 3)"},
+                     "peak_source": "measured live: gfp_probe_imad_wide (pure IMAD.WIDE "
+                                    "issue rate, 8 independent chains/thread, best of 3)"},
         "roofline_hbm": {"bound": "hbm", "achieved": hbm_bytes / (ms * 1e-3) / 1e9,
                          "peak": hbm_peak, "unit": "GB/s",
                          "frac": hbm_bytes / (ms * 1e-3) / 1e9 / hbm_peak,

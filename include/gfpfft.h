@@ -165,8 +165,8 @@ int gfp_fft_twiddle(const gfp_fft_plan *plan, const uint64_t *x, uint64_t *out, 
    plan (instrumentation for the benchmark's gpu_launches count). */
 int64_t gfp_fft_plan_last_launches(const gfp_fft_plan *plan);
 
-/* Instrumentation: run `iters` x 8 independent mad.wide.s32 chains per
-   thread on a blocks x threads grid and report the kernel time and the
+/* Instrumentation: run `iters` x 8 independent IMAD.WIDE (32x32 -> 64)
+   product chains per thread on a blocks x threads grid and report the kernel time and the
    number of IMAD.WIDE executed -- the measured integer-pipe peak the
    benchmark's roofline divides by. */
 int gfp_probe_imad_wide(int64_t iters, int blocks, int threads, float *ms_out, double *ops_out,

@@ -66,24 +66,11 @@ GFP_D u64 column_quot(i64 LL, i64 MID, i64 HH, const RadixConsts &rc, u64 &rem)
 // limb split: the negation of a balanced limb pair is again a balanced limb
 // pair, so it costs one IMAD per limb instead of a 64-bit negate.
 template <int KD, bool SPARSE>
-GFP_D void fast_mul_lazy(const i64 (&x)[KD], const i64 (&y)[KD], i64 (&f)[KD],
-                         const RadixConsts &rc, unsigned negx = 0)
+GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&xs)[KD],
+                          const int (&yl)[KD], const int (&yh)[KD], const int (&ys)[KD],
+                          i64 (&f)[KD], const RadixConsts &rc)
 {
     constexpr int S = FastSplit<KD>::S;
-    constexpr i64 half = (i64)1 << (S - 1);
-    int xl[KD], xh[KD], xs[KD], yl[KD], yh[KD], ys[KD];
-#pragma unroll
-    for (int i = 0; i < KD; i++) {
-        const int h0 = (int)((x[i] + half) >> S);
-        const int l0 = (int)(x[i] - ((i64)h0 << S));
-        const int sg = 1 - (int)((negx >> i) & 1u) * 2;
-        xh[i] = h0 * sg;
-        xl[i] = l0 * sg;
-        xs[i] = xl[i] + xh[i];
-        yh[i] = (int)((y[i] + half) >> S);
-        yl[i] = (int)(y[i] - ((i64)yh[i] << S));
-        ys[i] = yl[i] + yh[i];
-    }
     // Columns in order, with the two carry rounds streaming behind them:
     //   round 1  c_m = q_m r + d_m                       (column_quot)
     //   round 2  d_m + q_{m-1} = q2_m r + d2_m            (norm_bal)
@@ -129,4 +116,56 @@ GFP_D void fast_mul_lazy(const i64 (&x)[KD], const i64 (&y)[KD], i64 (&f)[KD],
     const int q2_0 = norm_bal<SPARSE>(d0 - q_prev, rc, d2_0);
     f[0] = d2_0 - q2_prev;
     f[1] = f1 + q2_0;
+}
+
+// balanced limb split of one digit: v = h 2^S + l, l in [-2^(S-1), 2^(S-1))
+template <int S>
+GFP_D void split_limbs(i64 v, int &l, int &h)
+{
+    constexpr i64 half = (i64)1 << (S - 1);
+    h = (int)((v + half) >> S);
+    l = (int)(v - ((i64)h << S));
+}
+
+template <int KD, bool SPARSE>
+GFP_D void fast_mul_lazy(const i64 (&x)[KD], const i64 (&y)[KD], i64 (&f)[KD],
+                         const RadixConsts &rc, unsigned negx = 0)
+{
+    constexpr int S = FastSplit<KD>::S;
+    int xl[KD], xh[KD], xs[KD], yl[KD], yh[KD], ys[KD];
+#pragma unroll
+    for (int i = 0; i < KD; i++) {
+        int l0, h0;
+        split_limbs<S>(x[i], l0, h0);
+        const int sg = 1 - (int)((negx >> i) & 1u) * 2;
+        xh[i] = h0 * sg;
+        xl[i] = l0 * sg;
+        xs[i] = xl[i] + xh[i];
+        split_limbs<S>(y[i], yl[i], yh[i]);
+        ys[i] = yl[i] + yh[i];
+    }
+    fast_mul_limbs<KD, SPARSE>(xl, xh, xs, yl, yh, ys, f, rc);
+}
+
+// the same product with y given as pre-split limb pairs (l | h << 32 per
+// digit, the plan's limb tables): no split work for the twiddle operand
+template <int KD, bool SPARSE>
+GFP_D void fast_mul_lazy_ylimbs(const i64 (&x)[KD], const u64 (&ylh)[KD], i64 (&f)[KD],
+                                const RadixConsts &rc, unsigned negx = 0)
+{
+    constexpr int S = FastSplit<KD>::S;
+    int xl[KD], xh[KD], xs[KD], yl[KD], yh[KD], ys[KD];
+#pragma unroll
+    for (int i = 0; i < KD; i++) {
+        int l0, h0;
+        split_limbs<S>(x[i], l0, h0);
+        const int sg = 1 - (int)((negx >> i) & 1u) * 2;
+        xh[i] = h0 * sg;
+        xl[i] = l0 * sg;
+        xs[i] = xl[i] + xh[i];
+        yl[i] = (int)(unsigned)ylh[i];
+        yh[i] = (int)(unsigned)(ylh[i] >> 32);
+        ys[i] = yl[i] + yh[i];
+    }
+    fast_mul_limbs<KD, SPARSE>(xl, xh, xs, yl, yh, ys, f, rc);
 }

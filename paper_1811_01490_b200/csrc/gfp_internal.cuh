@@ -23,7 +23,8 @@ int check_kr(int k, u64 r);
 struct PassArgs {
     const u64 *in;
     u64 *out;
-    const u64 *table;  // element-major [M][k] canonical, omega^b (or omega^b / N)
+    const u64 *table;  // element-major [M][k] balanced, omega^b (or omega^b / N)
+    const u64 *table_lh;  // the same entries as limb pairs l | h << 32 (k_pass44)
     const u64 *pre;    // optional pointwise operand, digit-major like `in`
     const u64 *in2;    // optional second set of `batch` vectors (grid.y >= batch)
     u64 *out2;
@@ -69,6 +70,8 @@ struct gfp_fft_plan {
     RadixConsts rc;
     u64 *table;       // element-major [M][k]: omega^b
     u64 *table_ninv;  // element-major [M][k]: omega^b * N^-1
+    u64 *table_lh;    // both tables as balanced limb pairs (k_pass44 only, else null)
+    u64 *table_ninv_lh;
     // host-path scratch
     u64 *h_dev;
     int64_t h_words;

@@ -265,6 +265,7 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
     A.in = in;
     A.out = out;
     A.table = scale ? p->table_ninv : p->table;
+    A.table_lh = scale ? p->table_ninv_lh : p->table_lh;
     A.pre = pre;
     A.batch_stride = (int64_t)KD * p->N;
     A.lN = ilog2_exact(p->N);

@@ -153,6 +153,23 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
         int64_t b = 0;
         unsigned negx = 0;
         const int64_t pos = j + ((int64_t)t << lM);
+        if (em_in) {
+            // first pass (Ns = 1, a = 0), element-major input, possibly mapped
+            // host memory: the warp's 32 elements (j0 .. j0 + 31, t) are 2 KB
+            // contiguous; read them with lane-contiguous 16 B loads (full
+            // 512 B requests over PCIe) into this row's smem slots
+            const int64_t j0 = (int64_t)blockIdx.x << 5;
+            const u64 *rowp = em_in + (j0 + ((int64_t)t << lM)) * KD;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int e = (lane >> 2) + 8 * q, dp = (lane & 3) * 2;
+                ulonglong2 v = make_ulonglong2(0, 0);
+                if (j0 + e < M && j0 + e + ((int64_t)t << lM) < n_in)
+                    v = reinterpret_cast<const ulonglong2 *>(rowp)[lane + 32 * q];
+                *reinterpret_cast<ulonglong2 *>(sm + (t * 32 + e) * SLOT + dp) = v;
+            }
+            __syncwarp();
+        }
         if (active) {
             // E = t (j mod Ns) (M / Ns) < N; omega^E = r^a omega^b
             int64_t E = ((int64_t)t * (j & nsmask)) << (lM - lNs);
@@ -166,25 +183,21 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
             // wrapped (d < a mod k) xor a >= k
             const int as = a & (KD - 1);
             negx = ((1u << as) - 1u) ^ (a >= KD ? ((1u << KD) - 1u) : 0u);
-            if (em_in) {  // first pass (a = 0): element-major, zero-padded past n_in
-                if (pos < n_in) {
-                    const ulonglong2 *ep = reinterpret_cast<const ulonglong2 *>(em_in + pos * KD);
+            if (em_in) {
+                const i64 *slot = sm + (t * 32 + lane) * SLOT;
 #pragma unroll
-                    for (int d = 0; d < KD; d += 2) {
-                        const ulonglong2 v = ep[d / 2];
-                        x[d] = (i64)v.x;
-                        x[d + 1] = (i64)v.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int d = 0; d < KD; d++)
-                        x[d] = 0;
+                for (int d = 0; d < KD; d += 2) {
+                    const longlong2 v = *reinterpret_cast<const longlong2 *>(slot + d);
+                    x[d] = v.x;
+                    x[d + 1] = v.y;
                 }
             } else {
+                // rows are N words apart; k N words fit 32-bit offsets (N <= 2^26)
                 const u64 *src = in + pos;
+                const unsigned rowN = 1u << lN;
 #pragma unroll
                 for (int d = 0; d < KD; d++)
-                    x[d] = (i64)__ldg(src + ((int64_t)((d - as) & (KD - 1)) << lN));
+                    x[d] = (i64)__ldg(src + (unsigned)((d - as) & (KD - 1)) * rowN);
             }
             if (A.in_canon)  // pass 0 only, where a = 0
                 to_balanced<KD>(x, rc.r);
@@ -200,15 +213,15 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
         // of r (b = 0) multiply by table[0] = 1 instead of diverging
         if (__any_sync(FULL_MASK, active && (b || A.scale))) {
             if (active) {
-                i64 y[KD];
-                const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(A.table + b * KD);
+                u64 ylh[KD];
+                const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(A.table_lh + b * KD);
 #pragma unroll
                 for (int d = 0; d < KD; d += 2) {
                     const ulonglong2 v = __ldg(tp + d / 2);
-                    y[d] = (i64)v.x;
-                    y[d + 1] = (i64)v.y;
+                    ylh[d] = v.x;
+                    ylh[d + 1] = v.y;
                 }
-                fast_mul_lazy<KD, SPARSE>(x, y, f, rc, negx);
+                fast_mul_lazy_ylimbs<KD, SPARSE>(x, ylh, f, rc, negx);
             }
         } else if (active) {
 #pragma unroll
@@ -275,6 +288,39 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
     case 2: p44::dft4<KD, INV, 2>(e[0], e[1], e[2], e[3]); break;
     default: p44::dft4<KD, INV, 3>(e[0], e[1], e[2], e[3]); break;
     }
+    if (em_out) {
+        // last pass (Ns = M: output u of group j at j + u M), element-major,
+        // possibly mapped host memory: park the canonical outputs in this
+        // warp's own stage-2 slots (rows 4 w + u1), then write each u's 32
+        // elements (2 KB contiguous) with lane-contiguous 16 B stores
+        const int64_t j0 = (int64_t)blockIdx.x << 5;
+#pragma unroll
+        for (int u1 = 0; u1 < 4; u1++) {
+            p44::normalize_el<KD, SPARSE>(e[u1], rc);
+            u64 c[KD];
+            lazy_to_canonical(e[u1], c, KD, rc);
+            i64 *slot = sm + ((4 * w + u1) * 32 + lane) * SLOT;
+#pragma unroll
+            for (int d = 0; d < KD; d += 2)
+                *reinterpret_cast<longlong2 *>(slot + d) = make_longlong2(c[d], c[d + 1]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u1 = 0; u1 < 4; u1++) {
+            const int64_t ubase = j0 + ((int64_t)(w + 4 * u1) << lM);
+            u64 *rowp = em_out + ubase * KD;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const int e = (lane >> 2) + 8 * q, dp = (lane & 3) * 2;
+                const longlong2 v =
+                    *reinterpret_cast<const longlong2 *>(sm + ((4 * w + u1) * 32 + e) * SLOT + dp);
+                if (j0 + e < M && ubase + e < A.n_out)
+                    reinterpret_cast<ulonglong2 *>(rowp)[lane + 32 * q] =
+                        make_ulonglong2((u64)v.x, (u64)v.y);
+            }
+        }
+        return;
+    }
     if (!active)
         return;
     // X[u0 + 4 u1] = e[u1] -> (j / Ns) Ns K + (j mod Ns) + u Ns
@@ -286,14 +332,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
         if (A.canon) {
             u64 c[KD];
             lazy_to_canonical(e[u1], c, KD, rc);
-            if (em_out) {  // last pass: element-major, the first n_out elements
-                if (pos < A.n_out) {
-                    ulonglong2 *ep = reinterpret_cast<ulonglong2 *>(em_out + pos * KD);
-#pragma unroll
-                    for (int d = 0; d < KD; d += 2)
-                        ep[d / 2] = make_ulonglong2(c[d], c[d + 1]);
-                }
-            } else {
+            {
 #pragma unroll
                 for (int d = 0; d < KD; d++)
                     out[((int64_t)d << lN) + pos] = c[d];

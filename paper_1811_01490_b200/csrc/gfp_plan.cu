@@ -84,6 +84,23 @@ __global__ void k_table_balance(u64 *__restrict__ tab, int64_t n, u64 r)
     }
 }
 
+// balanced table entries -> limb pairs (l | h << 32, v = h 2^S + l) for the
+// k_pass44 twiddle multiply (fast_mul_lazy_ylimbs)
+template <int KD>
+__global__ void k_table_limbs(const u64 *__restrict__ tab, u64 *__restrict__ out, int64_t n)
+{
+    constexpr int S = FastSplit<KD>::S;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n;
+         b += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int d = 0; d < KD; d++) {
+            int l, h;
+            split_limbs<S>((i64)tab[b * KD + d], l, h);
+            out[b * KD + d] = (u64)(unsigned)l | ((u64)(unsigned)h << 32);
+        }
+    }
+}
+
 // Four-step inter-stage twiddle (the sharded transform):
 // x is digit-major [batch][k][n] canonical; element (b, i) is multiplied by
 // omega^((row0 + b) i) (omega^-(...) when inverse), omega the plan's N-th
@@ -340,6 +357,18 @@ int gfp_fft_plan_create(gfp_fft_plan **plan, int k, uint64_t r, int K, int e,
     DISPATCH_FAST_K(k, (k_table_balance<KD><<<grid_for(p->M, 128), 128, 0, st>>>(p->table_ninv, p->M,
                                                                                 r)));
     err = cuda_status();
+    if (!err && em_io_supported(p)) {
+        if (cudaMalloc(&p->table_lh, tbytes) != cudaSuccess ||
+            cudaMalloc(&p->table_ninv_lh, tbytes) != cudaSuccess) {
+            err = GFP_ENOMEM;
+        } else {
+            DISPATCH_FAST_K(k, (k_table_limbs<KD><<<grid_for(p->M, 128), 128, 0, st>>>(
+                                   p->table, p->table_lh, p->M)));
+            DISPATCH_FAST_K(k, (k_table_limbs<KD><<<grid_for(p->M, 128), 128, 0, st>>>(
+                                   p->table_ninv, p->table_ninv_lh, p->M)));
+            err = cuda_status();
+        }
+    }
     if (!err && cudaStreamSynchronize(st) != cudaSuccess)
         err = GFP_ECUDA;
     cudaFree(d_sq);
@@ -347,6 +376,8 @@ int gfp_fft_plan_create(gfp_fft_plan **plan, int k, uint64_t r, int K, int e,
     if (err) {
         cudaFree(p->table);
         cudaFree(p->table_ninv);
+        cudaFree(p->table_lh);
+        cudaFree(p->table_ninv_lh);
         free(p);
         return err;
     }
@@ -380,6 +411,8 @@ int gfp_fft_plan_destroy(gfp_fft_plan *p)
         return GFP_OK;
     cudaFree(p->table);
     cudaFree(p->table_ninv);
+    cudaFree(p->table_lh);
+    cudaFree(p->table_ninv_lh);
     cudaFree(p->h_dev);
     free(p);
     return GFP_OK;

@@ -1,8 +1,8 @@
 // gfp_probe.cu -- instrumentation: measured integer-pipe peak for the
 // roofline ("IMAD.WIDE.U32 peak: to be measured on the box").
-// Each thread runs NCH independent mad.wide.s32 chains; the operands stay
-// 32-bit so ptxas cannot fold them, and the result is stored so nothing is
-// dead.  ops = grid * block * iters * NCH IMAD.WIDE per launch.
+// Each thread runs NCH independent chains of 32x32 -> 64 products (one
+// IMAD.WIDE each, nothing else in the loop); the result is stored so nothing
+// is dead.  ops = grid * block * iters * NCH IMAD.WIDE per launch.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -12,28 +12,33 @@
 
 __global__ void k_probe_imad_wide(int64_t iters, int a0, int b0, int64_t *out)
 {
-    int b = b0 ^ blockIdx.x;
-    int64_t acc[NCH];
+    // NCH independent chains of pure IMAD.WIDE: each 32x32 -> 64 product's
+    // high and low halves are the next multiplier and multiplicand, so ptxas
+    // emits exactly one IMAD.WIDE per product and nothing else in the loop
+    // (an accumulating mad.wide.s32 compiles on sm_100a to IMAD.WIDE + a
+    // 64-bit IADD3 pair, which would measure the ALU pipe as well).  This is
+    // the issue rate of the pipe the transform's limb products run on:
+    // 32 per clock per SM on B200.
+    int a[NCH], b[NCH];
 #pragma unroll
-    for (int c = 0; c < NCH; c++)
-        acc[c] = c + a0 + threadIdx.x;
+    for (int c = 0; c < NCH; c++) {
+        a[c] = a0 + c + threadIdx.x;
+        b[c] = (b0 ^ blockIdx.x) + c;
+    }
     for (int64_t i = 0; i < iters; i++) {
 #pragma unroll
         for (int c = 0; c < NCH; c++) {
-            // the multiplicand depends on the running accumulator, so the
-            // product cannot be hoisted out of the loop
             int64_t d;
-            asm volatile("{\n\t.reg .u32 t;\n\tcvt.u32.u64 t, %1;\n\t"
-                         "mad.wide.s32 %0, t, %2, %1;\n\t}"
-                         : "=l"(d) : "l"(acc[c]), "r"(b + c));
-            acc[c] = d;
+            asm volatile("mul.wide.s32 %0, %1, %2;" : "=l"(d) : "r"(a[c]), "r"(b[c]));
+            a[c] = (int)(d >> 32);
+            b[c] = (int)d;
         }
     }
-    int64_t s = 0;
+    int s = 0;
 #pragma unroll
     for (int c = 0; c < NCH; c++)
-        s ^= acc[c];
-    if (s == 0x123456789)
+        s ^= a[c] ^ b[c];
+    if (s == 0x12345678)
         out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
