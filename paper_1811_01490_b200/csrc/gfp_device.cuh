@@ -102,13 +102,26 @@ GFP_D i64 floordiv_small(i64 v, const RadixConsts &rc, i64 &rem)
     return q;
 }
 
-// 32x32 -> 64 signed multiply-add in one IMAD.WIDE (the compiler otherwise
-// may widen to a 64x64 multiply)
+// 32x32 -> 64 signed multiply-add, c + a b, as one IMAD.WIDE with a 64-bit
+// register addend.  Written as a carry chain over the two 32-bit halves
+// (mad.lo.cc.u32 + madc.hi.s32): ptxas fuses that pair into IMAD.WIDE with
+// the accumulator, whereas a chain of mad.wide.s32 is re-associated into
+// IMAD.WIDE ..., RZ products summed by IADD3 pairs -- one extra ALU
+// instruction per product on sm_100a, where the ALU pipe is the limit.
+template <bool CC = true>
 GFP_D i64 mad_wide_s32(int a, int b, i64 c)
 {
-    i64 d;
-    asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
-    return d;
+    if (!CC) {  // plain form (the k >= 16 kernels keep more registers free with it)
+        i64 d;
+        asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+        return d;
+    }
+    unsigned lo = (unsigned)c;
+    int hi = (int)(c >> 32);
+    asm("mad.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.s32 %1, %2, %3, %1;"
+        : "+r"(lo), "+r"(hi)
+        : "r"(a), "r"(b));
+    return (i64)(((u64)(unsigned)hi << 32) | lo);
 }
 
 // Balanced lazy normaliser: v = q r + rem with q small and

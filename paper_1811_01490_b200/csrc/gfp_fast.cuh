@@ -71,6 +71,7 @@ GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&
                           i64 (&f)[KD], const RadixConsts &rc)
 {
     constexpr int S = FastSplit<KD>::S;
+    constexpr bool CC = KD <= 8;  // fused-accumulate IMAD.WIDE form (gfp_device.cuh)
     // Columns in order, with the two carry rounds streaming behind them:
     //   round 1  c_m = q_m r + d_m                       (column_quot)
     //   round 2  d_m + q_{m-1} = q2_m r + d2_m            (norm_bal)
@@ -84,15 +85,15 @@ GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&
         i64 LL = 0, SS = 0, HH = 0, LLn = 0, SSn = 0, HHn = 0;
 #pragma unroll
         for (int i = 0; i <= m; i++) {
-            LL = mad_wide_s32(xl[i], yl[m - i], LL);
-            SS = mad_wide_s32(xs[i], ys[m - i], SS);
-            HH = mad_wide_s32(xh[i], yh[m - i], HH);
+            LL = mad_wide_s32<CC>(xl[i], yl[m - i], LL);
+            SS = mad_wide_s32<CC>(xs[i], ys[m - i], SS);
+            HH = mad_wide_s32<CC>(xh[i], yh[m - i], HH);
         }
 #pragma unroll
         for (int i = m + 1; i < KD; i++) {  // wrapped terms: r^k = -1
-            LLn = mad_wide_s32(xl[i], yl[m - i + KD], LLn);
-            SSn = mad_wide_s32(xs[i], ys[m - i + KD], SSn);
-            HHn = mad_wide_s32(xh[i], yh[m - i + KD], HHn);
+            LLn = mad_wide_s32<CC>(xl[i], yl[m - i + KD], LLn);
+            SSn = mad_wide_s32<CC>(xs[i], ys[m - i + KD], SSn);
+            HHn = mad_wide_s32<CC>(xh[i], yh[m - i + KD], HHn);
         }
         LL -= LLn;
         HH -= HHn;

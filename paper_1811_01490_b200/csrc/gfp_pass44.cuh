@@ -33,7 +33,7 @@
 #include "gfp_fast.cuh"
 
 #ifndef P44_MINB
-#define P44_MINB 5  // CTAs per SM the NW = 4 variant is register-bounded for
+#define P44_MINB 4  // CTAs per SM the NW = 4 variant is register-bounded for
 #endif
 
 namespace p44 {

@@ -129,6 +129,22 @@ __global__ void k_wide_acc(int64_t iters, int b0, int64_t *out) {
     if (s == 0x1234567) out[threadIdx.x] = s;
 }
 
+// IMAD.WIDE with a 64-bit register addend (the carry-chain formulation ptxas
+// fuses): independent accumulators, multiplier fed from the accumulator
+__global__ void k_wide_cc(int64_t iters, int b0, int64_t *out) {
+    unsigned lo[NCH]; int hi[NCH], a[NCH];
+    for (int c = 0; c < NCH; c++) { lo[c] = threadIdx.x + c; hi[c] = 0; a[c] = threadIdx.x * 3 + c; }
+    for (int64_t i = 0; i < iters; i++)
+#pragma unroll
+        for (int c = 0; c < NCH; c++) {
+            asm volatile("mad.lo.cc.u32 %0, %2, %3, %0;\n\tmadc.hi.s32 %1, %2, %3, %1;"
+                         : "+r"(lo[c]), "+r"(hi[c]) : "r"(a[c]), "r"(b0 + c));
+            a[c] = hi[c];
+        }
+    int64_t s = 0; for (int c = 0; c < NCH; c++) s ^= ((int64_t)hi[c] << 32) | lo[c];
+    if (s == 0x1234567) out[threadIdx.x] = s;
+}
+
 template <typename F>
 double run(F kern, const char *name, int sms, double mhz) {
     int64_t *out; cudaMalloc(&out, 1 << 20);
@@ -152,6 +168,7 @@ int main(int argc, char **argv) {
     int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     run(k_wide_rz, "IMAD.WIDE only", sms, mhz);
     run(k_wide_acc, "IMAD.WIDE+64b add", sms, mhz);
+    run(k_wide_cc, "IMAD.WIDE reg addend", sms, mhz);
     run(k_madwide_s32, "mad.wide.s32 chain", sms, mhz);
     run(k_madwide_u32, "mad.wide.u32 chain", sms, mhz);
     run(k_madwide_u32_ind, "mad.wide.u32 ind+lop", sms, mhz);

@@ -19,9 +19,11 @@ for log in sorted(glob.glob("paper_1811_01490_b200/csrc/*.ptxas.log")):
         m = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", line)
         if m:
             spill = "spill %s/%s" % m.groups()
-        m = re.search(r"Used (\d+) registers.*?(\d+) bytes smem", line)
+        m = re.search(r"Used (\d+) registers", line)
         if m and cur:
+            sm = re.search(r"(\d+) bytes smem", line)
             name = subprocess.run(["c++filt", cur], capture_output=True, text=True).stdout.strip()
             if pat in name:
-                print("%4s regs  %6s smem  %-16s %s" % (m.group(1), m.group(2), spill, name))
+                print("%4s regs  %6s smem  %-16s %s" % (m.group(1), sm.group(1) if sm else "0",
+                                                       spill, name))
             cur = None
