@@ -47,6 +47,13 @@ struct RadixConsts {
     int sp_eps;
     int q_sh1;      // max(w - 2S, 0) and max(2S - w, 0) for column_quot
     int q_sh2;
+    // mode 2 (r = 2^a + 2^b, the paper's radices): quotients by shifts only
+    int p2_ok;      // the mode's bounds hold (fast_bounds)
+    int p2_b;       // b = log2(eps)
+    int p2_sh;      // a - 2S (column_quot_p2)
+    int p2_ab;      // a - b
+    u64 p2_bias_t;  // (2^62 r) / 2^a = 2^62 + 2^(62 + b - a)
+    u64 p2_bias_lo; // (2^62 r) mod 2^64
 };
 
 // ---------------------------------------------------------------------------
@@ -130,9 +137,15 @@ GFP_D i64 mad_wide_s32(int a, int b, i64 c)
 // IMAD.WIDE:
 //   q = (v + 2^(a-1)) >> a,  rem = ((v + 2^(a-1)) mod 2^a) - 2^(a-1) - q eps;
 // otherwise a rounded division through a double estimate (one fix-up).
-template <bool SPARSE>
+template <int SPARSE>
 GFP_D int norm_bal(i64 v, const RadixConsts &rc, i64 &rem)
 {
+    if (SPARSE == 2) {  // eps = 2^b: q eps is a shift (ALU, not the IMAD pipe)
+        const i64 vb = v + rc.sp_half;
+        const int q = (int)(vb >> rc.sp_a);
+        rem = ((vb & rc.sp_mask) - rc.sp_half) - (i64)((u64)(i64)q << rc.p2_b);
+        return q;
+    }
     if (SPARSE) {
         const i64 vb = v + rc.sp_half;
         const int q = (int)(vb >> rc.sp_a);

@@ -164,6 +164,23 @@ RadixConsts make_consts(int k, u64 r)
         c.q_sh1 = c.w > 2 * c.s ? c.w - 2 * c.s : 0;
         c.q_sh2 = c.w < 2 * c.s ? 2 * c.s - c.w : 0;
         c.bias_t = r << (63 - c.w);
+        // mode 2: r = 2^a + 2^b, quotients by shifts (gfp_fast.cuh column_quot_p2)
+        const int a = fp.sp_a, S = c.s;
+        const i64 eps = fp.sp_eps;
+        if (fp.sp_on && eps > 0 && (eps & (eps - 1)) == 0 && a >= 2 * S && a - 2 * S < 32) {
+            const int b = __builtin_ctzll((u64)eps);
+            const u128 X = (u128)(r / 2) + fp.delta;
+            const u128 two62r = (u128)r << 62;
+            // |c| <= k X^2 < 2^62 r keeps c + 2^62 r in [0, 2^63 r): T < 2^64
+            if (62 + b - a >= 0 && (u128)k * X * X < two62r) {
+                c.p2_ok = 1;
+                c.p2_b = b;
+                c.p2_sh = a - 2 * S;
+                c.p2_ab = a - b;
+                c.p2_bias_t = ((u64)1 << 62) + ((u64)1 << (62 + b - a));
+                c.p2_bias_lo = (u64)two62r;
+            }
+        }
     } else {
         c.s = 0;
         c.stages_per_norm = 0;
@@ -269,7 +286,7 @@ __global__ void k_mul_generic(const u64 *__restrict__ x, const u64 *__restrict__
     }
 }
 
-template <int KD, bool SPARSE>
+template <int KD, int SPARSE>
 __global__ void k_mul_fast(const u64 *__restrict__ x, const u64 *__restrict__ y, int64_t y_inc,
                            u64 *__restrict__ z, int64_t n, RadixConsts rc)
 {

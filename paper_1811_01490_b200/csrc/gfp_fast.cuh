@@ -54,6 +54,24 @@ GFP_D u64 column_quot(i64 LL, i64 MID, i64 HH, const RadixConsts &rc, u64 &rem)
     return q;
 }
 
+// Mode 2 (r = 2^a + 2^b): with the bias B = 2^62 r (a multiple of 2^a),
+// T = floor((c + B) / 2^a) comes from shifts of the sub-columns, and
+// 1 / r = 2^-a (1 - 2^(b-a) + ...) gives the quotient estimate
+//   q = T - (T >> (a - b)) - 2,  floor((c + B) / r) - q in [0, 3],
+// so rem = (c + B) - q r (= low 64 bits minus two shifts) is in [0, 4r)
+// without a 64 x 64 multiply.  Returns the signed carry q - 2^62.
+template <int S>
+GFP_D i64 column_quot_p2(i64 LL, i64 MID, i64 HH, const RadixConsts &rc, u64 &rem)
+{
+    const i64 mid = MID + (LL >> S);                // floor(c / 2^S)
+    const i64 t2s = HH + (mid >> S);                 // floor(c / 2^(2S))
+    const u64 T = (u64)(t2s >> (rc.p2_sh & 31)) + rc.p2_bias_t;
+    const u64 q = T - (T >> (rc.p2_ab & 63)) - 2;
+    const u64 clo = (u64)LL + ((u64)MID << S) + ((u64)HH << (2 * S)) + rc.p2_bias_lo;
+    rem = clo - (q << (rc.sp_a & 63)) - (q << (rc.p2_b & 63));
+    return (i64)(q - (1ULL << 62));
+}
+
 // x * y mod p for balanced lazy digits (|digit| <= r/2 + delta), output
 // balanced lazy digits.  Limbs are balanced too, x = xh 2^S + xl with
 // xl in [-2^(S-1), 2^(S-1)), and the middle sub-column comes from one
@@ -65,10 +83,13 @@ GFP_D u64 column_quot(i64 LL, i64 MID, i64 HH, const RadixConsts &rc, u64 &rem)
 // rotation x * r^a, whose wrapped digits change sign (r^k = -1), into the
 // limb split: the negation of a balanced limb pair is again a balanced limb
 // pair, so it costs one IMAD per limb instead of a 64-bit negate.
-template <int KD, bool SPARSE>
+//
+// dst != nullptr: each output digit is stored to dst[m] as soon as it is
+// final instead of being kept in f (frees registers in the pass kernel).
+template <int KD, int SPARSE>
 GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&xs)[KD],
                           const int (&yl)[KD], const int (&yh)[KD], const int (&ys)[KD],
-                          i64 (&f)[KD], const RadixConsts &rc)
+                          i64 (&f)[KD], const RadixConsts &rc, i64 *dst = nullptr)
 {
     constexpr int S = FastSplit<KD>::S;
     constexpr bool CC = KD <= 8;  // fused-accumulate IMAD.WIDE form (gfp_device.cuh)
@@ -99,7 +120,13 @@ GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&
         HH -= HHn;
         const i64 MID = (SS - SSn) - LL - HH;
         u64 rem;
-        const u64 qq = column_quot<S>(LL, MID, HH, rc, rem);
+        i64 carry;
+        if (SPARSE == 2) {
+            carry = column_quot_p2<S>(LL, MID, HH, rc, rem);
+        } else {
+            const u64 qq = column_quot<S>(LL, MID, HH, rc, rem);
+            carry = (i64)(qq - (1ULL << 63));
+        }
         if (m == 0) {
             d0 = (i64)rem;
         } else {
@@ -108,15 +135,26 @@ GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&
             if (m == 1)
                 f1 = d2;  // + q2_0, known only after the last column
             else
-                f[m] = d2 + q2_prev;
+            {
+                const i64 v = d2 + q2_prev;
+                if (dst)
+                    dst[m] = v;
+                else
+                    f[m] = v;
+            }
             q2_prev = q2;
         }
-        q_prev = (i64)(qq - (1ULL << 63));
+        q_prev = carry;
     }
     i64 d2_0;
     const int q2_0 = norm_bal<SPARSE>(d0 - q_prev, rc, d2_0);
-    f[0] = d2_0 - q2_prev;
-    f[1] = f1 + q2_0;
+    if (dst) {
+        dst[0] = d2_0 - q2_prev;
+        dst[1] = f1 + q2_0;
+    } else {
+        f[0] = d2_0 - q2_prev;
+        f[1] = f1 + q2_0;
+    }
 }
 
 // balanced limb split of one digit: v = h 2^S + l, l in [-2^(S-1), 2^(S-1))
@@ -128,7 +166,7 @@ GFP_D void split_limbs(i64 v, int &l, int &h)
     l = (int)(v - ((i64)h << S));
 }
 
-template <int KD, bool SPARSE>
+template <int KD, int SPARSE>
 GFP_D void fast_mul_lazy(const i64 (&x)[KD], const i64 (&y)[KD], i64 (&f)[KD],
                          const RadixConsts &rc, unsigned negx = 0)
 {
@@ -150,9 +188,9 @@ GFP_D void fast_mul_lazy(const i64 (&x)[KD], const i64 (&y)[KD], i64 (&f)[KD],
 
 // the same product with y given as pre-split limb pairs (l | h << 32 per
 // digit, the plan's limb tables): no split work for the twiddle operand
-template <int KD, bool SPARSE>
+template <int KD, int SPARSE>
 GFP_D void fast_mul_lazy_ylimbs(const i64 (&x)[KD], const u64 (&ylh)[KD], i64 (&f)[KD],
-                                const RadixConsts &rc, unsigned negx = 0)
+                                const RadixConsts &rc, unsigned negx = 0, i64 *dst = nullptr)
 {
     constexpr int S = FastSplit<KD>::S;
     int xl[KD], xh[KD], xs[KD], yl[KD], yh[KD], ys[KD];
@@ -168,5 +206,5 @@ GFP_D void fast_mul_lazy_ylimbs(const i64 (&x)[KD], const u64 (&ylh)[KD], i64 (&
         yh[i] = (int)(unsigned)(ylh[i] >> 32);
         ys[i] = yl[i] + yh[i];
     }
-    fast_mul_limbs<KD, SPARSE>(xl, xh, xs, yl, yh, ys, f, rc);
+    fast_mul_limbs<KD, SPARSE>(xl, xh, xs, yl, yh, ys, f, rc, dst);
 }

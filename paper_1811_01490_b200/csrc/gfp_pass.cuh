@@ -25,7 +25,7 @@ GFP_D i64 rot_lane(i64 val, int t, int d, bool inverse)
 
 // one lazy normalisation of a digit held one-digit-per-lane: the quotient
 // moves one lane up (negated into digit 0: r^k = -1)
-template <int KD, bool SPARSE>
+template <int KD, int SPARSE>
 GFP_D void normalize_lane(i64 &v, int d, const RadixConsts &rc)
 {
     i64 rem;
@@ -50,7 +50,7 @@ __host__ __device__ constexpr int bitrev_c(int x)
 // omega^E, E = t (j mod Ns) (M / Ns), and writes the K-point DFT to
 // (j / Ns) Ns K + (j mod Ns) + u Ns.  After log_K N passes the output is the
 // natural-order DFT (the reference's dft_general result, fft.py:298-360).
-template <int KD, bool SPARSE>
+template <int KD, int SPARSE>
 __global__ void __launch_bounds__(256) k_pass(PassArgs A)
 {
     constexpr int K = 2 * KD;

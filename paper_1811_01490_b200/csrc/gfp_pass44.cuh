@@ -93,7 +93,7 @@ GFP_D void dft4(i64 (&x0)[KD], i64 (&x1)[KD], i64 (&x2)[KD], i64 (&x3)[KD])
 
 // one balanced normalisation of a lazy element: digit quotients move one
 // digit up, the top one wraps negated into digit 0 (r^k = -1)
-template <int KD, bool SPARSE>
+template <int KD, int SPARSE>
 GFP_D void normalize_el(i64 (&v)[KD], const RadixConsts &rc)
 {
     int q[KD];
@@ -109,7 +109,7 @@ GFP_D void normalize_el(i64 (&v)[KD], const RadixConsts &rc)
 
 }  // namespace p44
 
-template <int KD, bool SPARSE, bool INV, int NW>
+template <int KD, int SPARSE, bool INV, int NW>
 __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1) k_pass44(PassArgs A)
 {
     static_assert(KD == 8, "radix 4 x 4 pass is for K = 16");
@@ -209,8 +209,13 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
                 fast_mul_lazy<KD, SPARSE>(x, y, x, rc);
             }
         }
+        // element t parks in slot t: holding four elements in registers
+        // across the multiplies would cost occupancy
+        i64 *slot = sm + (t * 32 + lane) * SLOT;
         // the multiply is warp-uniform: lanes whose twiddle is a pure power
-        // of r (b = 0) multiply by table[0] = 1 instead of diverging
+        // of r (b = 0) multiply by table[0] = 1 instead of diverging; it
+        // stores each product digit to the slot as soon as it is final
+        bool parked = false;
         if (__any_sync(FULL_MASK, active && (b || A.scale))) {
             if (active) {
                 u64 ylh[KD];
@@ -221,7 +226,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
                     ylh[d] = v.x;
                     ylh[d + 1] = v.y;
                 }
-                fast_mul_lazy_ylimbs<KD, SPARSE>(x, ylh, f, rc, negx);
+                fast_mul_lazy_ylimbs<KD, SPARSE>(x, ylh, f, rc, negx, slot);
+                parked = true;
             }
         } else if (active) {
 #pragma unroll
@@ -233,12 +239,11 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
             for (int d = 0; d < KD; d++)
                 f[d] = 0;
         }
-        // park element t in slot t: holding four elements in registers
-        // across the multiplies would cost occupancy
-        i64 *slot = sm + (t * 32 + lane) * SLOT;
+        if (!parked) {
 #pragma unroll
-        for (int d = 0; d < KD; d += 2)
-            *reinterpret_cast<longlong2 *>(slot + d) = make_longlong2(f[d], f[d + 1]);
+            for (int d = 0; d < KD; d += 2)
+                *reinterpret_cast<longlong2 *>(slot + d) = make_longlong2(f[d], f[d + 1]);
+        }
     }
 
     // ---- stage 1 (warps w < 4, t1 = w): 4-point DFT over t2 (root rho^4) of
@@ -384,17 +389,18 @@ static int launch_pass44(const PassArgs &A, int64_t M, int64_t nsets, cudaStream
     case 8: k_pass44<KD, SP, IV, 8><<<grid, 256, 0, st>>>(A); break;                          \
     default: k_pass44<KD, SP, IV, 16><<<grid, 512, 0, st>>>(A); break;                        \
     }
-        if (A.rc.sp_on) {
+        // mode 2 (shift quotients) for r = 2^a + 2^b, else the generic mode
+        if (A.rc.p2_ok) {
             if (inv) {
-                P44_LAUNCH(true, true)
+                P44_LAUNCH(2, true)
             } else {
-                P44_LAUNCH(true, false)
+                P44_LAUNCH(2, false)
             }
         } else {
             if (inv) {
-                P44_LAUNCH(false, true)
+                P44_LAUNCH(0, true)
             } else {
-                P44_LAUNCH(false, false)
+                P44_LAUNCH(0, false)
             }
         }
 #undef P44_LAUNCH

@@ -106,7 +106,7 @@ __global__ void k_table_limbs(const u64 *__restrict__ tab, u64 *__restrict__ out
 // omega^((row0 + b) i) (omega^-(...) when inverse), omega the plan's N-th
 // root, using the plan's table omega^j (j < N/K) and the cheap split
 // omega^E = (omega^(N/K))^a omega^j as a digit rotation.  Canonical output.
-template <int KD, bool SPARSE>
+template <int KD, int SPARSE>
 __global__ void k_twiddle_rows(const u64 *__restrict__ x, u64 *__restrict__ out,
                                const u64 *__restrict__ table, int64_t batch, int64_t n,
                                int64_t row0, int lN, int lM, int inverse, int root_inv,
