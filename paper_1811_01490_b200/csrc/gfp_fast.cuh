@@ -25,6 +25,11 @@
 #pragma once
 #include "gfp_device.cuh"
 
+// largest k whose multiply uses the fused-accumulate IMAD.WIDE form
+#ifndef GFP_CC_MAXK
+#define GFP_CC_MAXK 8
+#endif
+
 // limb split used by the fast multiply for each k (compile time; the host
 // bound check in gfp_kernels.cu:fast_bounds verifies it for the given r)
 template <int KD>
@@ -92,7 +97,7 @@ GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&
                           i64 (&f)[KD], const RadixConsts &rc, i64 *dst = nullptr)
 {
     constexpr int S = FastSplit<KD>::S;
-    constexpr bool CC = KD <= 8;  // fused-accumulate IMAD.WIDE form (gfp_device.cuh)
+    constexpr bool CC = KD <= GFP_CC_MAXK;  // fused-accumulate IMAD.WIDE form (gfp_device.cuh)
     // Columns in order, with the two carry rounds streaming behind them:
     //   round 1  c_m = q_m r + d_m                       (column_quot)
     //   round 2  d_m + q_{m-1} = q2_m r + d2_m            (norm_bal)

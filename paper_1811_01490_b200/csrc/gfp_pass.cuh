@@ -51,7 +51,7 @@ __host__ __device__ constexpr int bitrev_c(int x)
 // (j / Ns) Ns K + (j mod Ns) + u Ns.  After log_K N passes the output is the
 // natural-order DFT (the reference's dft_general result, fft.py:298-360).
 template <int KD, int SPARSE>
-__global__ void __launch_bounds__(256) k_pass(PassArgs A)
+__global__ void __launch_bounds__(KD >= 16 ? 128 : 256, KD == 16 ? 3 : 1) k_pass(PassArgs A)
 {
     constexpr int K = 2 * KD;
     constexpr int LK = KD == 4 ? 3 : KD == 8 ? 4 : KD == 16 ? 5 : 6;
@@ -79,46 +79,45 @@ __global__ void __launch_bounds__(256) k_pass(PassArgs A)
     const u64 *pre = A.pre ? A.pre + bidx * A.batch_stride : nullptr;
     const RadixConsts rc = A.rc;
 
-    // ---- phase A: load K elements per group, twiddle / pointwise multiply
+    // ---- phase A: load K elements per group, twiddle / pointwise multiply.
+    // omega^E = r^a omega^b: r^a is folded into the digit addressing of the
+    // load (digit d comes from row (d - a) mod k) and the wrapped digits'
+    // signs into the multiply's limb split (fast_mul_lazy negx); the product
+    // digits go straight to the element's shared-memory row.
 #pragma unroll 1
     for (int h = 0; h < 2; h++) {
         const int g = tid & (G - 1);
         const int t = (tid >> lG) + h * KD;
         const int64_t j = j0 + g;
+        const bool active = j < M;
+        const int64_t pos = j + ((int64_t)t << lM);
         i64 x[KD];
-        int a = 0;
-        if (j < M) {
-            const int64_t pos = j + ((int64_t)t << lM);
-#pragma unroll
-            for (int d = 0; d < KD; d++)
-                x[d] = (i64)__ldg(in + ((int64_t)d << lN) + pos);
-            if (A.in_canon)
-                to_balanced<KD>(x, rc.r);
-            if (pre) {
-                i64 y[KD];
-#pragma unroll
-                for (int d = 0; d < KD; d++)
-                    y[d] = (i64)__ldg(pre + ((int64_t)d << lN) + pos);
-                fast_mul_lazy<KD, SPARSE>(x, y, x, rc);
-            }
+        int64_t b = 0;
+        unsigned negx = 0;
+        if (active) {
             // E = t (j mod Ns) (M / Ns) < N; omega^E = (omega^M)^a omega^b
             int64_t E = ((int64_t)t * (j & nsmask)) << (lM - lNs);
             if (A.neg_exp && E)
                 E = N - E;
-            a = (int)(E >> lM);
-            const int64_t b = E & (M - 1);
+            int a = (int)(E >> lM);
+            b = E & (M - 1);
             // omega^M is r (or 1/r for plans built on an inverse root)
             if (A.root_inv && a)
                 a = 2 * KD - a;
-            if (b || A.scale) {
-                i64 y[KD];
-                const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(A.table + b * KD);
+            const int as = a & (KD - 1);
+            negx = (unsigned)(((1ull << as) - 1ull) ^ (a >= KD ? ((1ull << KD) - 1ull) : 0ull));
+            const u64 *src = in + pos;
+            const unsigned rowN = 1u << lN;
 #pragma unroll
-                for (int d = 0; d < KD; d += 2) {
-                    ulonglong2 w = __ldg(tp + d / 2);
-                    y[d] = (i64)w.x;
-                    y[d + 1] = (i64)w.y;
-                }
+            for (int d = 0; d < KD; d++)
+                x[d] = (i64)__ldg(src + (size_t)((unsigned)((d - as) & (KD - 1)) * rowN));
+            if (A.in_canon)  // pass 0 only, where a = 0
+                to_balanced<KD>(x, rc.r);
+            if (pre) {  // pass 0 only (a = b = 0)
+                i64 y[KD];
+#pragma unroll
+                for (int d = 0; d < KD; d++)
+                    y[d] = (i64)__ldg(pre + ((int64_t)d << lN) + pos);
                 fast_mul_lazy<KD, SPARSE>(x, y, x, rc);
             }
         } else {
@@ -126,21 +125,29 @@ __global__ void __launch_bounds__(256) k_pass(PassArgs A)
             for (int d = 0; d < KD; d++)
                 x[d] = 0;
         }
-        // x * r^a: rotation by a (0 <= a < 2k), wrapped digits negated
         i64 *row = sm + (((int64_t)t << lG) + g) * ROW;
+        // warp-uniform multiply: lanes with b = 0 multiply by table[0] = 1
+        if (__any_sync(FULL_MASK, active && (b || A.scale))) {
+            if (active) {
+                u64 ylh[KD];
+                const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(A.table_lh + b * KD);
 #pragma unroll
-        for (int d = 0; d < KD; d++) {
-            int p = d + a;
-            i64 v = x[d];
-            if (p >= KD) {
-                p -= KD;
-                v = -v;
+                for (int d = 0; d < KD; d += 2) {
+                    const ulonglong2 w = __ldg(tp + d / 2);
+                    ylh[d] = w.x;
+                    ylh[d + 1] = w.y;
+                }
+                i64 f[KD];
+                fast_mul_lazy_ylimbs<KD, SPARSE>(x, ylh, f, rc, negx, row);
+            } else {
+#pragma unroll
+                for (int d = 0; d < KD; d++)
+                    row[d] = 0;
             }
-            if (p >= KD) {
-                p -= KD;
-                v = -v;
-            }
-            row[p] = v;
+        } else {
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                row[d] = ((negx >> d) & 1u) ? -x[d] : x[d];
         }
     }
     __syncthreads();
@@ -216,9 +223,10 @@ __global__ void __launch_bounds__(256) k_pass(PassArgs A)
 
 static int pass_threads(int k, int64_t M, int *G_out)
 {
-    // groups per CTA: as many as fit 256 threads, fewer when the transform
-    // is too small to give every SM two CTAs
-    int Gmax = 256 / k;
+    // groups per CTA: as many as fit 256 threads (128 for k >= 16, whose
+    // multiply needs ~170 registers), fewer when the transform is too small
+    // to give every SM two CTAs
+    int Gmax = (k >= 16 ? 128 : 256) / k;
     int Gmin = 32 / k > 0 ? 32 / k : 1;
     static int g_env = -1;
     if (g_env < 0) {
@@ -255,10 +263,12 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
     size_t smem = pass_smem<KD>(G);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_pass<KD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)pass_smem<KD>(256 / KD));
-        cudaFuncSetAttribute(k_pass<KD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)pass_smem<KD>(256 / KD));
+        for (int m = 0; m < 3; m++) {
+            const void *fn = m == 0 ? (const void *)k_pass<KD, 0>
+                             : m == 1 ? (const void *)k_pass<KD, 1> : (const void *)k_pass<KD, 2>;
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)pass_smem<KD>(256 / KD));
+        }
         attr_set = true;
     }
     PassArgs A;
@@ -302,10 +312,12 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
     if (A.in_em || A.out_em)
         return GFP_EUNSUPPORTED;
     dim3 grid((unsigned)((p->M + G - 1) / G), (unsigned)(in2 ? 2 * batch : batch));
-    if (p->rc.sp_on) {
-        k_pass<KD, true><<<grid, threads, smem, st>>>(A);
+    if (p->rc.p2_ok) {
+        k_pass<KD, 2><<<grid, threads, smem, st>>>(A);
+    } else if (p->rc.sp_on) {
+        k_pass<KD, 1><<<grid, threads, smem, st>>>(A);
     } else {
-        k_pass<KD, false><<<grid, threads, smem, st>>>(A);
+        k_pass<KD, 0><<<grid, threads, smem, st>>>(A);
     }
     return cuda_status();
 }

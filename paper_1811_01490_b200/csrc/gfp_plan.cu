@@ -357,7 +357,7 @@ int gfp_fft_plan_create(gfp_fft_plan **plan, int k, uint64_t r, int K, int e,
     DISPATCH_FAST_K(k, (k_table_balance<KD><<<grid_for(p->M, 128), 128, 0, st>>>(p->table_ninv, p->M,
                                                                                 r)));
     err = cuda_status();
-    if (!err && em_io_supported(p)) {
+    if (!err) {  // limb-pair tables: the twiddle operand of every pass kernel
         if (cudaMalloc(&p->table_lh, tbytes) != cudaSuccess ||
             cudaMalloc(&p->table_ninv_lh, tbytes) != cudaSuccess) {
             err = GFP_ENOMEM;
