@@ -364,7 +364,7 @@ def run_ours(args, ws, rank, local):
     except ImportError:
         pass
 
-    # capture the poly-multiply in a CUDA graph (12 pass kernels)
+    # capture the poly-multiply in a CUDA graph (one launch per pass)
     direct()
     launches_per_step = int(lib.gfp_fft_plan_last_launches(plan.handle))
     graph = torch.cuda.CUDAGraph()
@@ -402,10 +402,10 @@ def run_ours(args, ws, rank, local):
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     traffic = None
-    try:
+    try:  # ncu --set full of the step's pass launches (tools/gpu_bench_profile.sh)
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = prof.get("c2_step_dram_bytes")
-    except (OSError, ValueError):
+        traffic = prof["c2"]["step_dram_bytes"]
+    except (OSError, ValueError, KeyError):
         pass
 
     # ---- e2e: host buffers through the C-ABI host entry point.  The
@@ -444,11 +444,14 @@ def run_ours(args, ws, rank, local):
         "config": {"workload": WORKLOADS["c2"]["name"], "k": k, "r": R[k], "K": K, "e": 4,
                    "N": N, "batch_per_gpu": 1, "parallelism": "replicas x%d" % ws,
                    "l2": "256 MiB buffer written between timed steps (inputs fit in L2)",
-                   "graph": "CUDA graph of the 12 pass kernels per step"},
-        "roofline": {"bound": "int", "kernel": "k_pass<8> (all launches of the step)",
+                   "graph": "CUDA graph of the %d pass kernels per step" % launches_per_step},
+        "roofline": {"bound": "int",
+                     "kernel": "k_pass44<8> (the %d pass launches of the step)" % launches_per_step,
                      "achieved": achieved / 1e12, "peak": peak_imad / 1e12,
                      "unit": "T IMAD.WIDE/s", "frac": achieved / peak_imad,
                      "traffic": traffic,
+                     "traffic_note": "dram read+write bytes per step, ncu --set full over the "
+                                     "step's pass launches (profiles/ncu_traffic.json)",
                      "algorithmic": "%d general multiplies x 3k^2 = %d IMAD.WIDE per step (executed; 4k^2 schoolbook limb products)"
                                     % (mults, imad),
                      "peak_source": "measured live: gfp_probe_imad_wide (pure IMAD.WIDE "

@@ -504,8 +504,12 @@ int gfp_vec_mul(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z
     cudaStream_t st = (cudaStream_t)stream;
     RadixConsts rc = make_consts(k, r);
     if (rc.stages_per_norm > 0) {
-        if (rc.sp_on) {
-            DISPATCH_FAST_K(k, (k_mul_fast<KD, true><<<grid_for(n, 128), 128, 0, st>>>(
+        // (mode 2 costs k = 32 registers it does not have: spills)
+        if (rc.p2_ok && k != 32) {
+            DISPATCH_FAST_K(k, (k_mul_fast<KD, 2><<<grid_for(n, 128), 128, 0, st>>>(
+                                   x, y, y_inc, z, n, rc)));
+        } else if (rc.sp_on) {
+            DISPATCH_FAST_K(k, (k_mul_fast<KD, 1><<<grid_for(n, 128), 128, 0, st>>>(
                                    x, y, y_inc, z, n, rc)));
         } else {
             DISPATCH_FAST_K(k, (k_mul_fast<KD, false><<<grid_for(n, 128), 128, 0, st>>>(

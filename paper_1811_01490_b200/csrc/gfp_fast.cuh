@@ -30,6 +30,10 @@
 #define GFP_CC_MAXK 8
 #endif
 
+#ifndef GFP_KARA_MAXK
+#define GFP_KARA_MAXK 32
+#endif
+
 // limb split used by the fast multiply for each k (compile time; the host
 // bound check in gfp_kernels.cu:fast_bounds verifies it for the given r)
 template <int KD>
@@ -98,6 +102,10 @@ GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&
 {
     constexpr int S = FastSplit<KD>::S;
     constexpr bool CC = KD <= GFP_CC_MAXK;  // fused-accumulate IMAD.WIDE form (gfp_device.cuh)
+    // limb Karatsuba (3 IMAD.WIDE per digit pair, 6 limb registers per
+    // digit) up to GFP_KARA_MAXK; above it the schoolbook form (4 IMAD.WIDE,
+    // 4 limb registers per digit) keeps the k = 32 operands in registers
+    constexpr bool KARA = KD <= GFP_KARA_MAXK;
     // Columns in order, with the two carry rounds streaming behind them:
     //   round 1  c_m = q_m r + d_m                       (column_quot)
     //   round 2  d_m + q_{m-1} = q2_m r + d2_m            (norm_bal)
@@ -109,21 +117,38 @@ GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&
 #pragma unroll
     for (int m = 0; m < KD; m++) {
         i64 LL = 0, SS = 0, HH = 0, LLn = 0, SSn = 0, HHn = 0;
+        if (KARA) {
 #pragma unroll
-        for (int i = 0; i <= m; i++) {
-            LL = mad_wide_s32<CC>(xl[i], yl[m - i], LL);
-            SS = mad_wide_s32<CC>(xs[i], ys[m - i], SS);
-            HH = mad_wide_s32<CC>(xh[i], yh[m - i], HH);
-        }
+            for (int i = 0; i <= m; i++) {
+                LL = mad_wide_s32<CC>(xl[i], yl[m - i], LL);
+                SS = mad_wide_s32<CC>(xs[i], ys[m - i], SS);
+                HH = mad_wide_s32<CC>(xh[i], yh[m - i], HH);
+            }
 #pragma unroll
-        for (int i = m + 1; i < KD; i++) {  // wrapped terms: r^k = -1
-            LLn = mad_wide_s32<CC>(xl[i], yl[m - i + KD], LLn);
-            SSn = mad_wide_s32<CC>(xs[i], ys[m - i + KD], SSn);
-            HHn = mad_wide_s32<CC>(xh[i], yh[m - i + KD], HHn);
+            for (int i = m + 1; i < KD; i++) {  // wrapped terms: r^k = -1
+                LLn = mad_wide_s32<CC>(xl[i], yl[m - i + KD], LLn);
+                SSn = mad_wide_s32<CC>(xs[i], ys[m - i + KD], SSn);
+                HHn = mad_wide_s32<CC>(xh[i], yh[m - i + KD], HHn);
+            }
+        } else {  // schoolbook limbs: SS accumulates the middle sub-column itself
+#pragma unroll
+            for (int i = 0; i <= m; i++) {
+                LL = mad_wide_s32<CC>(xl[i], yl[m - i], LL);
+                SS = mad_wide_s32<CC>(xl[i], yh[m - i], SS);
+                SS = mad_wide_s32<CC>(xh[i], yl[m - i], SS);
+                HH = mad_wide_s32<CC>(xh[i], yh[m - i], HH);
+            }
+#pragma unroll
+            for (int i = m + 1; i < KD; i++) {
+                LLn = mad_wide_s32<CC>(xl[i], yl[m - i + KD], LLn);
+                SSn = mad_wide_s32<CC>(xl[i], yh[m - i + KD], SSn);
+                SSn = mad_wide_s32<CC>(xh[i], yl[m - i + KD], SSn);
+                HHn = mad_wide_s32<CC>(xh[i], yh[m - i + KD], HHn);
+            }
         }
         LL -= LLn;
         HH -= HHn;
-        const i64 MID = (SS - SSn) - LL - HH;
+        const i64 MID = KARA ? (SS - SSn) - LL - HH : SS - SSn;
         u64 rem;
         i64 carry;
         if (SPARSE == 2) {

@@ -393,7 +393,11 @@ int gfp_fft_twiddle(const gfp_fft_plan *p, const uint64_t *x, uint64_t *out, int
     cudaStream_t st = (cudaStream_t)stream;
     const int lN = ilog2_exact(p->N), lM = ilog2_exact(p->M);
     dim3 grid = grid_for(batch * n, 128);
-    if (p->rc.sp_on) {
+    if (p->rc.p2_ok) {
+        DISPATCH_FAST_K(p->k, (k_twiddle_rows<KD, 2><<<grid, 128, 0, st>>>(
+                                  x, out, p->table, batch, n, row0, lN, lM, inverse ? 1 : 0,
+                                  p->root_inv, p->rc)));
+    } else if (p->rc.sp_on) {
         DISPATCH_FAST_K(p->k, (k_twiddle_rows<KD, true><<<grid, 128, 0, st>>>(
                                   x, out, p->table, batch, n, row0, lN, lM, inverse ? 1 : 0,
                                   p->root_inv, p->rc)));

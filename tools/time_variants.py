@@ -37,6 +37,14 @@ p16 = gp.GfpParams(R[16], 16); f16 = gp.GfpFftField(p16, backend="cuda")
 plan3 = gp.build_plan(f16, 32, 4, gp.roots_for(p16, 1 << 20))
 x = gp.vec.uniform(1 << 20, p16, seed=3, batch=8); y = torch.empty_like(x)
 res["c3x8_fwd_ms"] = timeit(lambda: gp.fft_tensor(x, plan3, out=y), 10)
+del x, y
+p32 = gp.GfpParams(R[32], 32); f32 = gp.GfpFftField(p32, backend="cuda")
+a = gp.vec.uniform(1 << 22, p32, seed=51); b = gp.vec.uniform(1 << 22, p32, seed=52)
+res["c5_mul_ms"] = timeit(lambda: gp.vec.mul(a, b, p32), 5)
+del a, b
+plan5 = gp.build_plan(f32, 64, 3, gp.roots_for(p32, 1 << 18))
+x = gp.vec.uniform(1 << 18, p32, seed=5); y = torch.empty_like(x)
+res["c5_fwd_ms"] = timeit(lambda: gp.fft_tensor(x, plan5, out=y), 10)
 print(json.dumps(res))
 ''' % ROOT
 
