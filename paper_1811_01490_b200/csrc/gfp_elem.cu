@@ -7,6 +7,7 @@
 #include "gfp_internal.cuh"
 #include "gfp_fast.cuh"
 #include "gfp_generic.cuh"
+#include "gfp_mulw.cuh"
 
 // ===========================================================================
 // host-side constants
@@ -503,6 +504,8 @@ int gfp_vec_mul(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z
         return e;
     cudaStream_t st = (cudaStream_t)stream;
     RadixConsts rc = make_consts(k, r);
+    if (launch_mul_wide(k, x, y, y_inc, z, n, rc, st))
+        return cuda_status();
     if (rc.stages_per_norm > 0) {
         // (mode 2 costs k = 32 registers it does not have: spills)
         if (rc.p2_ok && k != 32) {
