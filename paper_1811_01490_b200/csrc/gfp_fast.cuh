@@ -95,7 +95,7 @@ GFP_D i64 column_quot_p2(i64 LL, i64 MID, i64 HH, const RadixConsts &rc, u64 &re
 //
 // dst != nullptr: each output digit is stored to dst[m] as soon as it is
 // final instead of being kept in f (frees registers in the pass kernel).
-template <int KD, int SPARSE>
+template <int KD, int SPARSE, bool STORE = false>
 GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&xs)[KD],
                           const int (&yl)[KD], const int (&yh)[KD], const int (&ys)[KD],
                           i64 (&f)[KD], const RadixConsts &rc, i64 *dst = nullptr)
@@ -167,7 +167,7 @@ GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&
             else
             {
                 const i64 v = d2 + q2_prev;
-                if (dst)
+                if (STORE)
                     dst[m] = v;
                 else
                     f[m] = v;
@@ -178,7 +178,7 @@ GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&
     }
     i64 d2_0;
     const int q2_0 = norm_bal<SPARSE>(d0 - q_prev, rc, d2_0);
-    if (dst) {
+    if (STORE) {
         dst[0] = d2_0 - q2_prev;
         dst[1] = f1 + q2_0;
     } else {
@@ -218,7 +218,7 @@ GFP_D void fast_mul_lazy(const i64 (&x)[KD], const i64 (&y)[KD], i64 (&f)[KD],
 
 // the same product with y given as pre-split limb pairs (l | h << 32 per
 // digit, the plan's limb tables): no split work for the twiddle operand
-template <int KD, int SPARSE>
+template <int KD, int SPARSE, bool STORE = false>
 GFP_D void fast_mul_lazy_ylimbs(const i64 (&x)[KD], const u64 (&ylh)[KD], i64 (&f)[KD],
                                 const RadixConsts &rc, unsigned negx = 0, i64 *dst = nullptr)
 {
@@ -236,5 +236,91 @@ GFP_D void fast_mul_lazy_ylimbs(const i64 (&x)[KD], const u64 (&ylh)[KD], i64 (&
         yh[i] = (int)(unsigned)(ylh[i] >> 32);
         ys[i] = yl[i] + yh[i];
     }
-    fast_mul_limbs<KD, SPARSE>(xl, xh, xs, yl, yh, ys, f, rc, dst);
+    fast_mul_limbs<KD, SPARSE, STORE>(xl, xh, xs, yl, yh, ys, f, rc, dst);
+}
+
+// x * y with the y limbs in a shared-memory column (this thread's int2
+// {l, h} per digit at ywin[d * stride]; l + h formed as a digit enters) and only the x limbs in
+// registers: columns in blocks of four, x_i times the window
+// y_{m0-i} .. y_{m0+3-i} (mod k), one new y digit (negated when its index
+// wraps, r^k = -1) entering per step -- the k_mul_wide scheme
+// (gfp_mulw.cuh).  Product digits are stored to dst[m] as they become final.
+template <int KD, int SPARSE, bool CC>
+GFP_D void fast_mul_window_store(const i64 (&x)[KD], unsigned negx, const int2 *ywin, int stride,
+                                 i64 *dst, const RadixConsts &rc)
+{
+    constexpr int S = FastSplit<KD>::S;
+    int xl[KD], xh[KD], xs[KD];
+#pragma unroll
+    for (int i = 0; i < KD; i++) {
+        int l0, h0;
+        split_limbs<S>(x[i], l0, h0);
+        const int sg = 1 - (int)((negx >> i) & 1u) * 2;
+        xh[i] = h0 * sg;
+        xl[i] = l0 * sg;
+        xs[i] = xl[i] + xh[i];
+    }
+    i64 q_prev = 0, d0 = 0, f1 = 0;
+    int q2_prev = 0;
+#pragma unroll 1
+    for (int m0 = 0; m0 < KD; m0 += 4) {
+        i64 LL[4], SS[4], HH[4];
+#pragma unroll
+        for (int c = 0; c < 4; c++)
+            LL[c] = SS[c] = HH[c] = 0;
+        int4 win[4];
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const int2 v = ywin[(m0 + c) * stride];
+            win[c] = make_int4(v.x, v.y, v.x + v.y, 0);
+        }
+#pragma unroll
+        for (int i = 0; i < KD; i++) {
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                LL[c] = mad_wide_s32<CC>(xl[i], win[c].x, LL[c]);
+                HH[c] = mad_wide_s32<CC>(xh[i], win[c].y, HH[c]);
+                SS[c] = mad_wide_s32<CC>(xs[i], win[c].z, SS[c]);
+            }
+            if (i + 1 < KD) {
+#pragma unroll
+                for (int c = 3; c > 0; c--)
+                    win[c] = win[c - 1];
+                const int j = m0 - i - 1;
+                int2 v = ywin[((j + KD) & (KD - 1)) * stride];
+                if (j < 0)
+                    v = make_int2(-v.x, -v.y);
+                win[0] = make_int4(v.x, v.y, v.x + v.y, 0);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const int m = m0 + c;
+            const i64 MID = SS[c] - LL[c] - HH[c];
+            u64 rem;
+            i64 carry;
+            if (SPARSE == 2) {
+                carry = column_quot_p2<S>(LL[c], MID, HH[c], rc, rem);
+            } else {
+                const u64 qq = column_quot<S>(LL[c], MID, HH[c], rc, rem);
+                carry = (i64)(qq - (1ULL << 63));
+            }
+            if (m == 0) {
+                d0 = (i64)rem;
+            } else {
+                i64 d2;
+                const int q2 = norm_bal<SPARSE>((i64)rem + q_prev, rc, d2);
+                if (m == 1)
+                    f1 = d2;
+                else
+                    dst[m] = d2 + q2_prev;
+                q2_prev = q2;
+            }
+            q_prev = carry;
+        }
+    }
+    i64 d2_0;
+    const int q2_0 = norm_bal<SPARSE>(d0 - q_prev, rc, d2_0);
+    dst[0] = d2_0 - q2_prev;
+    dst[1] = f1 + q2_0;
 }

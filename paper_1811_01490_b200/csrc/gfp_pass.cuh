@@ -12,6 +12,22 @@
 #include "gfp_fast.cuh"
 #include "gfp_pass44.cuh"
 
+// k values whose pass multiply keeps the twiddle limbs in shared memory
+// (fast_mul_window_store) instead of registers
+#ifndef PASS_WINDOW_MINK
+#define PASS_WINDOW_MINK 16
+#endif
+#ifndef PASS_WINDOW_MAXK
+#define PASS_WINDOW_MAXK 16
+#endif
+#define PASS_WINDOW(KD) ((KD) >= PASS_WINDOW_MINK && (KD) <= PASS_WINDOW_MAXK)
+#ifndef GFP_WINDOW_CC
+#define GFP_WINDOW_CC true
+#endif
+#ifndef PASS16_MINB
+#define PASS16_MINB 3  // CTAs per SM the k = 16 pass is register-bounded for
+#endif
+
 template <int KD>
 GFP_D i64 rot_lane(i64 val, int t, int d, bool inverse)
 {
@@ -51,7 +67,8 @@ __host__ __device__ constexpr int bitrev_c(int x)
 // (j / Ns) Ns K + (j mod Ns) + u Ns.  After log_K N passes the output is the
 // natural-order DFT (the reference's dft_general result, fft.py:298-360).
 template <int KD, int SPARSE>
-__global__ void __launch_bounds__(KD >= 16 ? 128 : 256, KD == 16 ? 3 : 1) k_pass(PassArgs A)
+__global__ void __launch_bounds__(KD >= 16 ? 128 : 256, KD == 16 ? PASS16_MINB : 1)
+    k_pass(PassArgs A)
 {
     constexpr int K = 2 * KD;
     constexpr int LK = KD == 4 ? 3 : KD == 8 ? 4 : KD == 16 ? 5 : 6;
@@ -129,16 +146,33 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256, KD == 16 ? 3 : 1) k_pass
         // warp-uniform multiply: lanes with b = 0 multiply by table[0] = 1
         if (__any_sync(FULL_MASK, active && (b || A.scale))) {
             if (active) {
-                u64 ylh[KD];
                 const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(A.table_lh + b * KD);
+                if (PASS_WINDOW(KD)) {
+                    // twiddle limbs staged in this thread's smem column,
+                    // multiplied through the sliding window (registers: x only)
+                    // (a limb pair l | h << 32 is the int2 {l, h} bit for bit)
+                    unsigned long long *yw =
+                        reinterpret_cast<unsigned long long *>(sm + ((size_t)K << lG) * ROW) + tid;
+                    const int nt = (int)blockDim.x;
 #pragma unroll
-                for (int d = 0; d < KD; d += 2) {
-                    const ulonglong2 w = __ldg(tp + d / 2);
-                    ylh[d] = w.x;
-                    ylh[d + 1] = w.y;
+                    for (int d = 0; d < KD; d += 2) {
+                        const ulonglong2 w = __ldg(tp + d / 2);
+                        yw[d * nt] = w.x;
+                        yw[(d + 1) * nt] = w.y;
+                    }
+                    fast_mul_window_store<KD, SPARSE, GFP_WINDOW_CC>(
+                        x, negx, reinterpret_cast<const int2 *>(yw), nt, row, rc);
+                } else {
+                    u64 ylh[KD];
+#pragma unroll
+                    for (int d = 0; d < KD; d += 2) {
+                        const ulonglong2 w = __ldg(tp + d / 2);
+                        ylh[d] = w.x;
+                        ylh[d + 1] = w.y;
+                    }
+                    i64 f[KD];
+                    fast_mul_lazy_ylimbs<KD, SPARSE, true>(x, ylh, f, rc, negx, row);
                 }
-                i64 f[KD];
-                fast_mul_lazy_ylimbs<KD, SPARSE>(x, ylh, f, rc, negx, row);
             } else {
 #pragma unroll
                 for (int d = 0; d < KD; d++)
@@ -250,7 +284,10 @@ static int pass_threads(int k, int64_t M, int *G_out)
 template <int KD>
 static size_t pass_smem(int G)
 {
-    return (size_t)(2 * KD) * G * (KD + 1) * sizeof(i64);
+    // [K][G][k + 1] element rows, plus the window multiply's y-limb columns
+    // (k int2 per thread, G k threads) when it is on for this k
+    return (size_t)(2 * KD) * G * (KD + 1) * sizeof(i64) +
+           (PASS_WINDOW(KD) ? (size_t)KD * G * KD * sizeof(int2) : 0);
 }
 
 template <int KD>

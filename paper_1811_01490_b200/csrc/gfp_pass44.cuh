@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
                     ylh[d] = v.x;
                     ylh[d + 1] = v.y;
                 }
-                fast_mul_lazy_ylimbs<KD, SPARSE>(x, ylh, f, rc, negx, slot);
+                fast_mul_lazy_ylimbs<KD, SPARSE, true>(x, ylh, f, rc, negx, slot);
                 parked = true;
             }
         } else if (active) {
