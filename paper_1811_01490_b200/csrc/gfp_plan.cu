@@ -481,6 +481,13 @@ static int ensure_host_scratch(gfp_fft_plan *p, int64_t words)
 // no transpose kernel).  Pageable memory returns nullptr: the caller stages.
 static u64 *mapped_alias(const void *h)
 {
+    static int zc = -1;
+    if (zc < 0) {
+        const char *e = getenv("GFP_ZERO_COPY");  // experiment hook: 0 = stage with DMA copies
+        zc = (e && e[0] == '0') ? 0 : 1;
+    }
+    if (!zc)
+        return nullptr;
     cudaPointerAttributes at;
     if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
         cudaGetLastError();
