@@ -38,6 +38,32 @@
 
 namespace p44 {
 
+// digit rotation a (0 <= a < 2k) of element t of group j in a pass:
+// omega^E = r^a omega^b, E = t (j mod Ns)(M / Ns)
+struct Twiddle {
+    int64_t b;
+    int as;
+    unsigned negx;
+};
+template <int KD>
+GFP_D Twiddle twiddle_of(int t, int64_t j, int64_t nsmask, int lM, int lNs, int64_t N,
+                         int64_t M, int neg_exp, int root_inv)
+{
+    Twiddle tw;
+    int64_t E = ((int64_t)t * (j & nsmask)) << (lM - lNs);
+    if (neg_exp && E)
+        E = N - E;
+    int a = (int)(E >> lM);
+    tw.b = E & (M - 1);
+    if (root_inv && a)
+        a = 2 * KD - a;
+    // x * r^a: digit d comes from row (d - a) mod k, negated when it
+    // wrapped (d < a mod k) xor a >= k
+    tw.as = a & (KD - 1);
+    tw.negx = ((1u << tw.as) - 1u) ^ (a >= KD ? ((1u << KD) - 1u) : 0u);
+    return tw;
+}
+
 // y = x * r^S for a compile-time S in [0, 2k): digit renaming, wrapped
 // digits negated (r^k = -1)
 template <int KD, int S>
@@ -171,18 +197,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
             __syncwarp();
         }
         if (active) {
-            // E = t (j mod Ns) (M / Ns) < N; omega^E = r^a omega^b
-            int64_t E = ((int64_t)t * (j & nsmask)) << (lM - lNs);
-            if (A.neg_exp && E)
-                E = N - E;
-            int a = (int)(E >> lM);
-            b = E & (M - 1);
-            if (A.root_inv && a)
-                a = 2 * KD - a;
-            // x * r^a: digit d comes from row (d - a) mod k, negated when it
-            // wrapped (d < a mod k) xor a >= k
-            const int as = a & (KD - 1);
-            negx = ((1u << as) - 1u) ^ (a >= KD ? ((1u << KD) - 1u) : 0u);
+            const p44::Twiddle tw = p44::twiddle_of<KD>(t, j, nsmask, lM, lNs, N, M,
+                                                        A.neg_exp, A.root_inv);
+            b = tw.b;
+            negx = tw.negx;
             if (em_in) {
                 const i64 *slot = sm + (t * 32 + lane) * SLOT;
 #pragma unroll
@@ -196,8 +214,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
                 const u64 *src = in + pos;
                 const unsigned rowN = 1u << lN;
 #pragma unroll
-                for (int d = 0; d < KD; d++)
-                    x[d] = (i64)__ldg(src + (unsigned)((d - as) & (KD - 1)) * rowN);
+                for (int d = 0; d < KD; d++)  // streamed once: evict-first, keep the tables in L2
+                    x[d] = (i64)__ldcs(src + (unsigned)((d - tw.as) & (KD - 1)) * rowN);
             }
             if (A.in_canon)  // pass 0 only, where a = 0
                 to_balanced<KD>(x, rc.r);
@@ -326,6 +344,46 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
         }
         return;
     }
+    if (lNs == 0) {
+        // first pass (Ns = 1): output u of group j goes to 16 j + u, so a
+        // lane-per-group store would scatter 8 B per 128 B line.  Park the
+        // outputs digit-major ([d][g][u], row pitch 17: conflict-free both
+        // ways) over the slots, then write each digit row's 512 consecutive
+        // positions lane-contiguously.
+        const int64_t j0 = (int64_t)blockIdx.x << 5;
+        i64 *park = sm;
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // stage-2 slot reads done
+#pragma unroll
+        for (int u1 = 0; u1 < 4; u1++) {
+            p44::normalize_el<KD, SPARSE>(e[u1], rc);
+            const int u = w + 4 * u1;
+            if (A.canon) {
+                u64 c[KD];
+                lazy_to_canonical(e[u1], c, KD, rc);
+#pragma unroll
+                for (int d = 0; d < KD; d++)
+                    park[(d * 32 + lane) * 17 + u] = (i64)c[d];
+            } else {
+#pragma unroll
+                for (int d = 0; d < KD; d++)
+                    park[(d * 32 + lane) * 17 + u] = e[u1][d];
+            }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int tid = threadIdx.x;  // < 128: the four stage-2 warps
+        u64 *obase = out + (j0 << 4);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; q4++) {
+            const int q = tid + 128 * q4;      // position 16 j0 + q
+            const int g = q >> 4, u = q & 15;  // group j0 + g, output u
+            if (j0 + g < M) {
+#pragma unroll
+                for (int d = 0; d < KD; d++)
+                    __stcs(obase + ((int64_t)d << lN) + q, (u64)park[(d * 32 + g) * 17 + u]);
+            }
+        }
+        return;
+    }
     if (!active)
         return;
     // X[u0 + 4 u1] = e[u1] -> (j / Ns) Ns K + (j mod Ns) + u Ns
@@ -340,12 +398,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
             {
 #pragma unroll
                 for (int d = 0; d < KD; d++)
-                    out[((int64_t)d << lN) + pos] = c[d];
+                    __stcs(out + ((int64_t)d << lN) + pos, c[d]);
             }
         } else {
 #pragma unroll
             for (int d = 0; d < KD; d++)
-                out[((int64_t)d << lN) + pos] = (u64)e[u1][d];
+                __stcs(out + ((int64_t)d << lN) + pos, (u64)e[u1][d]);
         }
     }
 }
