@@ -170,6 +170,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
     const int64_t j = ((int64_t)blockIdx.x << 5) + lane;
     const bool active = j < M;
 
+    // programmatic dependent launch: let the next pass's CTAs be scheduled
+    // as this grid drains, and wait for the previous pass's writes before the
+    // first global access (no-ops when launched without the attribute)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
     // ---- phase A: load + twiddle elements t = w + NW i (16 / NW per thread)
     i64 e[4][KD];
 #pragma unroll 1
@@ -419,6 +425,34 @@ static inline bool pass44_enabled(int k, const RadixConsts &rc)
     return k == 8 && !disabled && rc.stages_per_norm >= 4;
 }
 
+// launch with programmatic stream serialisation (PDL): the kernel may start
+// while the previous kernel on the stream drains; it orders itself with
+// griddepcontrol.wait.  GFP_PDL=0 launches plainly.
+static inline void launch_pdl(void (*kern)(PassArgs), dim3 grid, int threads, cudaStream_t st,
+                              const PassArgs &A)
+{
+    static int pdl = -1;
+    if (pdl < 0) {
+        const char *e = getenv("GFP_PDL");
+        pdl = (e && e[0] == '0') ? 0 : 1;
+    }
+    if (!pdl) {
+        kern<<<grid, threads, 0, st>>>(A);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, A);
+}
+
 // launcher: returns 1 when it handled the pass
 template <int KD>
 static int launch_pass44(const PassArgs &A, int64_t M, int64_t nsets, cudaStream_t st)
@@ -443,9 +477,9 @@ static int launch_pass44(const PassArgs &A, int64_t M, int64_t nsets, cudaStream
         const bool inv = A.rot_inv != 0;
 #define P44_LAUNCH(SP, IV)                                                                    \
     switch (nw) {                                                                             \
-    case 4: k_pass44<KD, SP, IV, 4><<<grid, 128, 0, st>>>(A); break;                          \
-    case 8: k_pass44<KD, SP, IV, 8><<<grid, 256, 0, st>>>(A); break;                          \
-    default: k_pass44<KD, SP, IV, 16><<<grid, 512, 0, st>>>(A); break;                        \
+    case 4: launch_pdl(k_pass44<KD, SP, IV, 4>, grid, 128, st, A); break;                     \
+    case 8: launch_pdl(k_pass44<KD, SP, IV, 8>, grid, 256, st, A); break;                     \
+    default: launch_pdl(k_pass44<KD, SP, IV, 16>, grid, 512, st, A); break;                   \
     }
         // mode 2 (shift quotients) for r = 2^a + 2^b, else the generic mode
         if (A.rc.p2_ok) {
