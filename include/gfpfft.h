@@ -124,6 +124,19 @@ int64_t gfp_fft_workspace_words(const gfp_fft_plan *plan, int64_t batch);
 int gfp_fft_exec(const gfp_fft_plan *plan, const uint64_t *in, uint64_t *out, uint64_t *work,
                  int64_t batch, int inverse, void *stream);
 
+/* gfp_fft_exec with the digit forms chosen by the caller and, optionally,
+   the four-step inter-stage twiddle of an enclosing transform folded into
+   the first pass: with ft != NULL, element (b, i) of the batch is first
+   multiplied by w^((ft_row0 + b) i) (w^-(...) if ft_inverse), w the root of
+   plan `ft` (same k; exponents mod ft's N) -- the D_{N1,N2} stage of the
+   reference's tensor formula (fft.py:62-103) without a separate pass.
+   in_canon = 0: the input is balanced lazy (the output of a call with
+   out_canon = 0), required when ft is given.  GFP_EUNSUPPORTED if this k's
+   pass kernel cannot fold the twiddle (then use gfp_fft_twiddle). */
+int gfp_fft_exec_ex(const gfp_fft_plan *plan, const uint64_t *in, uint64_t *out, uint64_t *work,
+                    int64_t batch, int inverse, int in_canon, int out_canon,
+                    const gfp_fft_plan *ft, int64_t ft_row0, int ft_inverse, void *stream);
+
 /* Cyclic product of length N: out = IDFT(DFT(f) .* DFT(g)), the polynomial
    product when deg f + deg g < N (the reference composes
    it from dft_general, GfpFftField.mul and dft_inverse). */

@@ -47,6 +47,8 @@ SIGNATURES = {
     "gfp_fft_plan_size": (_i64, [_vp]),
     "gfp_fft_workspace_words": (_i64, [_vp, _i64]),
     "gfp_fft_exec": (_int, [_vp, _u64p, _u64p, _u64p, _i64, _int, _vp]),
+    "gfp_fft_exec_ex": (_int, [_vp, _u64p, _u64p, _u64p, _i64, _int, _int, _int, _vp, _i64,
+                               _int, _vp]),
     "gfp_poly_mul": (_int, [_vp, _u64p, _u64p, _u64p, _u64p, _i64, _vp]),
     "gfp_fft_exec_host": (_int, [_vp, _u64p, _i64, _int, _vp]),
     "gfp_poly_mul_host": (_int, [_vp, _u64p, _u64p, _u64p, _i64, _vp]),

@@ -20,6 +20,8 @@ dim3 grid_for(int64_t work, int threads);
 int cuda_status();
 int check_kr(int k, u64 r);
 
+struct gfp_fft_plan;
+
 struct PassArgs {
     const u64 *in;
     u64 *out;
@@ -49,15 +51,27 @@ struct PassArgs {
     int64_t n_in, n_in2;
     u64 *out_em;
     int64_t n_out;
+    // four-step twiddle on the first pass (PassIO::ft): table (limb pairs),
+    // log2 of its plan's N and M, row offset, direction, plan root form
+    const u64 *ft_lh;
+    int ft_lN, ft_lM, ft_inv, ft_root_inv;
+    int64_t ft_row0;
 };
 
-// element-major endpoints of one transform (see PassArgs)
-struct EmIO {
+// Extras of one transform's first / last pass (k_pass44 only):
+// element-major endpoints (see PassArgs), and the four-step inter-stage
+// twiddle folded into the first pass: element (b, i) of the batch is
+// multiplied by w^(+-(ft_row0 + b) i), w the root of the plan `ft` (the
+// D_{N1,N2} stage of a sharded transform, fft.py:62-103).
+struct PassIO {
     const u64 *in;
     const u64 *in2;
     int64_t n_in, n_in2;
     u64 *out;
     int64_t n_out;
+    const gfp_fft_plan *ft;
+    int64_t ft_row0;
+    int ft_inv;
 };
 
 // ---------------------------------------------------------------------------
@@ -80,7 +94,7 @@ struct gfp_fft_plan {
 };
 
 // one radix-K Stockham pass (gfp_pass.cuh), instantiated per k in gfp_pass_k*.cu
-// true when the pass kernels of this plan take element-major I/O (EmIO)
+// true when the pass kernels of this plan take element-major I/O (PassIO)
 bool em_io_supported(const gfp_fft_plan *p);
 
 // em: element-major first-pass input / last-pass output (nullptr: none);
@@ -89,7 +103,7 @@ bool em_io_supported(const gfp_fft_plan *p);
 template <int KD>
 int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2, u64 *out2,
                 const u64 *pre, int64_t batch, int64_t Ns, int inverse, int scale, int canon,
-                int in_canon, const EmIO *em, cudaStream_t st);
+                int in_canon, const PassIO *em, cudaStream_t st);
 
 #define DISPATCH_K(k, CALL)                                                                     \
     switch (k) {                                                                                \

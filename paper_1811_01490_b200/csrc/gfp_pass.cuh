@@ -293,7 +293,7 @@ static size_t pass_smem(int G)
 template <int KD>
 int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
                        u64 *out2, const u64 *pre, int64_t batch, int64_t Ns, int inverse,
-                       int scale, int canon, int in_canon, const EmIO *em, cudaStream_t st)
+                       int scale, int canon, int in_canon, const PassIO *em, cudaStream_t st)
 {
     int G;
     int threads = pass_threads(KD, p->M, &G);
@@ -332,7 +332,20 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
     A.in_em = A.in2_em = nullptr;
     A.out_em = nullptr;
     A.n_in = A.n_in2 = A.n_out = 0;
+    A.ft_lh = nullptr;
+    A.ft_lN = A.ft_lM = A.ft_inv = A.ft_root_inv = 0;
+    A.ft_row0 = 0;
     if (em) {
+        if (Ns == 1 && em->ft && (scale || in_canon))
+            return GFP_EUNSUPPORTED;  // first pass with N^-1 or canonical input
+        if (Ns == 1 && em->ft) {
+            A.ft_lh = em->ft->table_lh;
+            A.ft_lN = ilog2_exact(em->ft->N);
+            A.ft_lM = ilog2_exact(em->ft->M);
+            A.ft_inv = em->ft_inv;
+            A.ft_root_inv = em->ft->root_inv;
+            A.ft_row0 = em->ft_row0;
+        }
         if (Ns == 1 && em->in) {
             A.in_em = em->in;
             A.in2_em = em->in2;
@@ -346,7 +359,7 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
     }
     if (launch_pass44<KD>(A, p->M, in2 ? 2 * batch : batch, st))
         return cuda_status();
-    if (A.in_em || A.out_em)
+    if (A.in_em || A.out_em || A.ft_lh)
         return GFP_EUNSUPPORTED;
     dim3 grid((unsigned)((p->M + G - 1) / G), (unsigned)(in2 ? 2 * batch : batch));
     if (p->rc.p2_ok) {

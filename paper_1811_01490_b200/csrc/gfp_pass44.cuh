@@ -203,8 +203,22 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
             __syncwarp();
         }
         if (active) {
-            const p44::Twiddle tw = p44::twiddle_of<KD>(t, j, nsmask, lM, lNs, N, M,
-                                                        A.neg_exp, A.root_inv);
+            p44::Twiddle tw = p44::twiddle_of<KD>(t, j, nsmask, lM, lNs, N, M,
+                                                  A.neg_exp, A.root_inv);
+            if (A.ft_lh) {
+                // first pass (own twiddle trivial): the four-step twiddle
+                // w^(+-(row0 + b) pos) of the enclosing transform instead
+                const int64_t Nf = (int64_t)1 << A.ft_lN;
+                int64_t E = ((A.ft_row0 + bidx) * pos) & (Nf - 1);
+                if (A.ft_inv && E)
+                    E = Nf - E;
+                int a = (int)(E >> A.ft_lM);
+                tw.b = E & (((int64_t)1 << A.ft_lM) - 1);
+                if (A.ft_root_inv && a)
+                    a = 2 * KD - a;
+                tw.as = a & (KD - 1);
+                tw.negx = ((1u << tw.as) - 1u) ^ (a >= KD ? ((1u << KD) - 1u) : 0u);
+            }
             b = tw.b;
             negx = tw.negx;
             if (em_in) {
@@ -243,7 +257,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
         if (__any_sync(FULL_MASK, active && (b || A.scale))) {
             if (active) {
                 u64 ylh[KD];
-                const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(A.table_lh + b * KD);
+                const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(
+                    (A.ft_lh ? A.ft_lh : A.table_lh) + b * KD);
 #pragma unroll
                 for (int d = 0; d < KD; d += 2) {
                     const ulonglong2 v = __ldg(tp + d / 2);

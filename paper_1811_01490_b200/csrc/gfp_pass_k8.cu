@@ -3,7 +3,7 @@
 #include "gfp_pass.cuh"
 
 template int launch_pass<8>(const gfp_fft_plan *, const u64 *, u64 *, const u64 *, u64 *,
-                             const u64 *, int64_t, int64_t, int, int, int, int, const EmIO *,
+                             const u64 *, int64_t, int64_t, int, int, int, int, const PassIO *,
                              cudaStream_t);
 
 bool em_io_supported(const gfp_fft_plan *p) { return pass44_enabled(p->k, p->rc); }

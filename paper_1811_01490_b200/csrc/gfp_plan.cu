@@ -176,7 +176,7 @@ __global__ void k_twiddle_rows(const u64 *__restrict__ x, u64 *__restrict__ out,
 // pass (single set only).
 static int run_transform2(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, const u64 *in_b,
                           u64 *out_b, u64 *work_b, const u64 *pre, int64_t batch, int inverse,
-                          int in_canon, int out_canon, cudaStream_t st, const EmIO *em = nullptr)
+                          int in_canon, int out_canon, cudaStream_t st, const PassIO *em = nullptr)
 {
     // ping-pong so that the last pass lands in `out`; inputs are never written
     int e = p->e;
@@ -220,7 +220,7 @@ static int run_transform2(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, c
 
 static int run_transform(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, const u64 *pre,
                          int64_t batch, int inverse, int in_canon, int out_canon,
-                         cudaStream_t st, const EmIO *em = nullptr)
+                         cudaStream_t st, const PassIO *em = nullptr)
 {
     return run_transform2(p, in, out, work, nullptr, nullptr, nullptr, pre, batch, inverse,
                           in_canon, out_canon, st, em);
@@ -442,6 +442,21 @@ int gfp_fft_exec(const gfp_fft_plan *cp, const uint64_t *in, uint64_t *out, uint
                          (cudaStream_t)stream);
 }
 
+int gfp_fft_exec_ex(const gfp_fft_plan *cp, const uint64_t *in, uint64_t *out, uint64_t *work,
+                    int64_t batch, int inverse, int in_canon, int out_canon,
+                    const gfp_fft_plan *ft, int64_t ft_row0, int ft_inverse, void *stream)
+{
+    gfp_fft_plan *p = const_cast<gfp_fft_plan *>(cp);
+    if (!p || !in || !out || !work || batch < 1 || ft_row0 < 0)
+        return GFP_EINVAL;
+    if (ft && (in_canon || ft->k != p->k || !em_io_supported(p)))
+        return ft->k != p->k || in_canon ? GFP_EINVAL : GFP_EUNSUPPORTED;
+    p->last_launches = 0;
+    PassIO io = {nullptr, nullptr, 0, 0, nullptr, 0, ft, ft_row0, ft_inverse ? 1 : 0};
+    return run_transform(p, in, out, work, nullptr, batch, inverse ? 1 : 0, in_canon ? 1 : 0,
+                         out_canon ? 1 : 0, (cudaStream_t)stream, ft ? &io : nullptr);
+}
+
 int gfp_poly_mul(const gfp_fft_plan *cp, const uint64_t *f, const uint64_t *g, uint64_t *out,
                  uint64_t *work, int64_t batch, void *stream)
 {
@@ -572,12 +587,12 @@ int gfp_poly_mul_host2(gfp_fft_plan *p, const uint64_t *f, int64_t nf, const uin
     u64 *dout = mo ? mo : stg;
     // forward transforms of both operands in the same launches; pass 0 reads
     // the element-major operands (zero past nf / ng); spectra stay lazy
-    EmIO e1 = {mf, mg, nf, ng, nullptr, 0};
+    PassIO e1 = {mf, mg, nf, ng, nullptr, 0, nullptr, 0, 0};
     err = run_transform2(p, F, F, s1, G, G, s2, nullptr, batch, 0, 1, 0, st, &e1);
     if (!err) {
         // inverse of F .* G (pointwise product fused into pass 0, N^-1 into
         // the last pass), which writes the first n_out elements element-major
-        EmIO e2 = {nullptr, nullptr, 0, 0, dout, n_out};
+        PassIO e2 = {nullptr, nullptr, 0, 0, dout, n_out, nullptr, 0, 0};
         err = run_transform(p, F, F, s1, G, batch, 1, 0, 1, st, &e2);
     }
     if (!err && !mo) {
@@ -633,7 +648,7 @@ int gfp_fft_exec_host(gfp_fft_plan *p, uint64_t *v, int64_t batch, int inverse, 
         p->last_launches += 2 * batch;
         cudaMemcpyAsync(v, a, sizeof(u64) * vw, cudaMemcpyDeviceToHost, st);
     } else {
-        EmIO em = {src, nullptr, N, 0, stage_out ? a : mv, N};
+        PassIO em = {src, nullptr, N, 0, stage_out ? a : mv, N, nullptr, 0, 0};
         err = run_transform(p, b, b, w, nullptr, batch, inverse ? 1 : 0, 1, 1, st, &em);
         if (err)
             return err;

@@ -62,21 +62,35 @@ class ShardedFFT:
     def forward(self, cols):
         """cols [N2/G, k, N1] (canonical) -> rows [N1/G, k, N2] (canonical)."""
         G, k, c1, c2 = self.world, self.k, self.c1, self.c2
-        y = self.ops.fft(cols, "N1", inverse=False)                  # A[n2l, d, k1]
-        y = self.ops.twiddle(y, self.rank * c2, inverse=False)        # * w_N^(n2 k1)
+        fused = getattr(self.ops, "fused", False)
+        if fused:  # lazy digits through the exchange, twiddle folded into the row DFT
+            y = self.ops.fft_ex(cols, "N1", inverse=False, in_canon=True, out_canon=False)
+        else:
+            y = self.ops.fft(cols, "N1", inverse=False)               # A[n2l, d, k1]
+            y = self.ops.twiddle(y, self.rank * c2, inverse=False)    # * w_N^(n2 k1)
         send = _i64(y).view(c2, k, G, c1).permute(2, 0, 1, 3).contiguous()
         recv = self._all_to_all(send)                                  # [g, n2l, d, k1l]
         rows = recv.permute(3, 2, 0, 1).reshape(c1, k, self.N2).contiguous()
+        if fused:  # * w_N^(k1 n2) on the row DFT's first pass
+            return self.ops.fft_ex(_u64(rows), "N2", inverse=False, in_canon=False,
+                                   out_canon=True, ft_row0=self.rank * c1)
         return self.ops.fft(_u64(rows), "N2", inverse=False)
 
     # -- inverse ----------------------------------------------------------
     def inverse(self, rows):
         """rows [N1/G, k, N2] -> cols [N2/G, k, N1]; inverse of forward()."""
         G, k, c1, c2 = self.world, self.k, self.c1, self.c2
-        z = self.ops.fft(rows, "N2", inverse=True)                   # B[k1l, d, n2]
+        fused = getattr(self.ops, "fused", False)
+        if fused:
+            z = self.ops.fft_ex(rows, "N2", inverse=True, in_canon=True, out_canon=False)
+        else:
+            z = self.ops.fft(rows, "N2", inverse=True)               # B[k1l, d, n2]
         send = _i64(z).view(c1, k, G, c2).permute(2, 0, 1, 3).contiguous()
         recv = self._all_to_all(send)                                  # [g, k1l, d, n2l]
         cols = recv.permute(3, 2, 0, 1).reshape(c2, k, self.N1).contiguous()
+        if fused:  # * w_N^-(n2 k1) on the column inverse DFT's first pass
+            return self.ops.fft_ex(_u64(cols), "N1", inverse=True, in_canon=False,
+                                   out_canon=True, ft_row0=self.rank * c2, ft_inverse=True)
         cols = self.ops.twiddle(_u64(cols), self.rank * c2, inverse=True)
         return self.ops.fft(cols, "N1", inverse=True)
 
@@ -112,10 +126,35 @@ class GpuShardOps:
         self.plans = {"N1": F.build_plan(field, K, e(N1), w1),
                       "N2": F.build_plan(field, K, e(N2), w2)}
         self.params = params
+        # the k_pass44 kernels fold the inter-stage twiddle into the next
+        # transform's first pass (gfp_fft_exec_ex); other k use the
+        # separate twiddle kernel
+        self.fused = params.k == 8 and min(e(N1), e(N2)) >= 2  # (single-pass plans
+        # would carry N^-1 and the twiddle in one pass: unfused)
 
     def fft(self, x, which, inverse):
         from .fft import fft
         return fft(x.contiguous(), self.plans[which], inverse=inverse)
+
+    def fft_ex(self, x, which, inverse, in_canon, out_canon, ft_row0=None, ft_inverse=False):
+        """Batched transform with chosen digit forms; ft_row0 folds the
+        four-step twiddle w_N^(+-(ft_row0 + b) i) into the first pass."""
+        import ctypes
+        from . import _lib
+        x = x.contiguous()
+        plan = self.plans[which]
+        B = x.shape[0]
+        out = torch.empty_like(x)
+        work = torch.empty(int(_lib.load().gfp_fft_workspace_words(plan.handle, B)),
+                           dtype=torch.uint64, device=x.device)
+        vp = ctypes.c_void_p
+        _lib.check(_lib.load().gfp_fft_exec_ex(
+            plan.handle, vp(x.data_ptr()), vp(out.data_ptr()), vp(work.data_ptr()), B,
+            1 if inverse else 0, 1 if in_canon else 0, 1 if out_canon else 0,
+            vp(self.plan_N.handle) if ft_row0 is not None else None,
+            ft_row0 if ft_row0 is not None else 0, 1 if ft_inverse else 0,
+            vp(torch.cuda.current_stream().cuda_stream)), "gfp_fft_exec_ex")
+        return out
 
     def twiddle(self, x, row0, inverse):
         import ctypes
