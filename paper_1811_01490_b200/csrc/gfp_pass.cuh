@@ -95,6 +95,9 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256, KD == 16 ? PASS16_MINB :
     u64 *out = out_base + bidx * A.batch_stride;
     const u64 *pre = A.pre ? A.pre + bidx * A.batch_stride : nullptr;
     const RadixConsts rc = A.rc;
+    // programmatic dependent launch (see k_pass44)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     // ---- phase A: load K elements per group, twiddle / pointwise multiply.
     // omega^E = r^a omega^b: r^a is folded into the digit addressing of the
@@ -363,11 +366,11 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
         return GFP_EUNSUPPORTED;
     dim3 grid((unsigned)((p->M + G - 1) / G), (unsigned)(in2 ? 2 * batch : batch));
     if (p->rc.p2_ok) {
-        k_pass<KD, 2><<<grid, threads, smem, st>>>(A);
+        launch_pdl(k_pass<KD, 2>, grid, threads, st, A, smem);
     } else if (p->rc.sp_on) {
-        k_pass<KD, 1><<<grid, threads, smem, st>>>(A);
+        launch_pdl(k_pass<KD, 1>, grid, threads, st, A, smem);
     } else {
-        k_pass<KD, 0><<<grid, threads, smem, st>>>(A);
+        launch_pdl(k_pass<KD, 0>, grid, threads, st, A, smem);
     }
     return cuda_status();
 }

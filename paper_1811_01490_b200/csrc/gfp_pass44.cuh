@@ -444,7 +444,7 @@ static inline bool pass44_enabled(int k, const RadixConsts &rc)
 // while the previous kernel on the stream drains; it orders itself with
 // griddepcontrol.wait.  GFP_PDL=0 launches plainly.
 static inline void launch_pdl(void (*kern)(PassArgs), dim3 grid, int threads, cudaStream_t st,
-                              const PassArgs &A)
+                              const PassArgs &A, size_t smem = 0)
 {
     static int pdl = -1;
     if (pdl < 0) {
@@ -452,13 +452,13 @@ static inline void launch_pdl(void (*kern)(PassArgs), dim3 grid, int threads, cu
         pdl = (e && e[0] == '0') ? 0 : 1;
     }
     if (!pdl) {
-        kern<<<grid, threads, 0, st>>>(A);
+        kern<<<grid, threads, smem, st>>>(A);
         return;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(threads);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
