@@ -262,7 +262,10 @@ GFP_D void fast_mul_window_store(const i64 (&x)[KD], unsigned negx, const int2 *
     }
     i64 q_prev = 0, d0 = 0, f1 = 0;
     int q2_prev = 0;
-#pragma unroll 1
+    // fully unrolled up to k = 16 (compile-time window addresses and wrap
+    // signs); k = 32 keeps the block loop to bound the code size
+    constexpr int UNR = KD <= 16 ? KD / 4 : 1;
+#pragma unroll UNR
     for (int m0 = 0; m0 < KD; m0 += 4) {
         i64 LL[4], SS[4], HH[4];
 #pragma unroll
