@@ -54,6 +54,9 @@ struct RadixConsts {
     int p2_ab;      // a - b
     u64 p2_bias_t;  // (2^62 r) / 2^a = 2^62 + 2^(62 + b - a)
     u64 p2_bias_lo; // (2^62 r) mod 2^64
+    // mode 3: r is the paper's radix for k (P2Radix<k>, compile-time a, b) and
+    // the sequential-carry bounds hold (ColReduce, gfp_fast.cuh)
+    int p3_ok;
 };
 
 // ---------------------------------------------------------------------------
@@ -131,15 +134,53 @@ GFP_D i64 mad_wide_s32(int a, int b, i64 c)
     return (i64)(((u64)(unsigned)hi << 32) | lo);
 }
 
+// Compile-time form of mode 2 for the paper's radices (DEFAULT_RADIX,
+// bench_cli.py:36-41): r = 2^a + 2^b with a, b known to the compiler, so
+// every shift by a or b and every bias is an immediate (a 64-bit shift by
+// a >= 32 is one SHF of the high word) -- SPARSE == 3 in the kernels.  The
+// arithmetic is identical to mode 2 (same bounds, fast_bounds).
+template <int KD>
+struct P2Radix {
+    static constexpr int a = 0, b = 0;
+};
+template <>
+struct P2Radix<8> {
+    static constexpr int a = 59, b = 16;
+};
+template <>
+struct P2Radix<16> {
+    static constexpr int a = 58, b = 10;
+};
+template <>
+struct P2Radix<32> {
+    static constexpr int a = 56, b = 21;
+};
+// r of the compile-time mode for k (0: none)
+GFP_HD constexpr u64 p2_radix_of(int k)
+{
+    return k == 8 ? (1ULL << 59) + (1ULL << 16)
+         : k == 16 ? (1ULL << 58) + (1ULL << 10)
+         : k == 32 ? (1ULL << 56) + (1ULL << 21) : 0;
+}
+
 // Balanced lazy normaliser: v = q r + rem with q small and
 // rem in [-r/2 - ex, r/2 + ex] (the host bound check fixes ex).  For the
 // paper's sparse radices r = 2^a + eps it is a shift, a mask and one
 // IMAD.WIDE:
 //   q = (v + 2^(a-1)) >> a,  rem = ((v + 2^(a-1)) mod 2^a) - 2^(a-1) - q eps;
 // otherwise a rounded division through a double estimate (one fix-up).
-template <int SPARSE>
+template <int SPARSE, int KD = 0>
 GFP_D int norm_bal(i64 v, const RadixConsts &rc, i64 &rem)
 {
+    if constexpr (SPARSE == 3) {  // compile-time r = 2^a + 2^b
+        constexpr int a = P2Radix<KD>::a, b = P2Radix<KD>::b;
+        static_assert(a >= 33 && b >= 1 && b < 32, "P2Radix");
+        constexpr i64 half = (i64)1 << (a - 1), mask = ((i64)1 << a) - 1;
+        const i64 vb = v + half;
+        const int q = (int)(vb >> a);
+        rem = (vb & mask) - half - ((i64)q << b);
+        return q;
+    }
     if (SPARSE == 2) {  // eps = 2^b: q eps is a shift (ALU, not the IMAD pipe)
         const i64 vb = v + rc.sp_half;
         const int q = (int)(vb >> rc.sp_a);
@@ -322,4 +363,44 @@ GFP_D void lazy_to_canonical(const DF &f, DZ &z, int k, const RadixConsts &rc)
         z[i] = (u64)t;
     }
     finish_canonical(z, k, rc.r, C);
+}
+
+// The same canonicalisation for a compile-time k, branch-free (selects
+// instead of the data-dependent loops above): the transform's last pass runs
+// it for every output, and the branchy form is ~1000 SASS instructions per
+// inlined copy.  Input: lazy digits with |f_i| < r - 1 (balanced or lazy).
+template <int KD>
+GFP_D void lazy_to_canonical_bf(const i64 (&f)[KD], u64 (&z)[KD], const RadixConsts &rc)
+{
+    const i64 r = (i64)rc.r;
+    int C = 0;
+#pragma unroll
+    for (int i = 0; i < KD; i++) {
+        i64 t = f[i] + C;
+        const bool neg = t < 0, ge = t >= r;
+        t = neg ? t + r : (ge ? t - r : t);
+        C = neg ? -1 : (ge ? 1 : 0);
+        z[i] = (u64)t;
+    }
+    // value = Z - C mod p: C = 1 subtracts 1 (borrow through zero digits),
+    // C = -1 adds 1 (carry through r - 1 digits); a borrow or carry out of the
+    // top digit means the value is p - 1 (form B).  Rare (|C| = 1 needs the
+    // top digit to overflow): kept out of the common path.
+    if (C != 0) {
+        bool bo = C == 1, ca = C == -1;
+#pragma unroll
+        for (int i = 0; i < KD; i++) {
+            const u64 v = z[i];
+            const bool z0 = v == 0, zt = v == rc.r - 1;
+            z[i] = bo ? (z0 ? rc.r - 1 : v - 1) : (ca ? (zt ? 0 : v + 1) : v);
+            bo = bo && z0;
+            ca = ca && zt;
+        }
+        if (bo || ca) {
+#pragma unroll
+            for (int i = 0; i < KD - 1; i++)
+                z[i] = 0;
+            z[KD - 1] = rc.r;
+        }
+    }
 }

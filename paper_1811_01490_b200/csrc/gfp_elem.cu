@@ -182,6 +182,30 @@ RadixConsts make_consts(int k, u64 r)
                 c.p2_bias_lo = (u64)two62r;
             }
         }
+        // mode 3 (ColReduce): column c_m + C_{m-1} with the running carry
+        // |C| <= k X^2 / r + small folded into LL before the signed quotient
+        if (c.p2_ok && r == p2_radix_of(k)) {
+            const int b = c.p2_b;
+            const u128 two63 = (u128)1 << 63;
+            const u128 X = (u128)(r / 2) + fp.delta;
+            const u128 half = (u128)1 << (S - 1);
+            const u128 H = (X + half) >> S;
+            const u128 kk = (u128)k;
+            const u128 cmax = kk * X * X / r + (kk * X * X / r >> 30) + 16;
+            const u128 cabs = kk * X * X + cmax;
+            const int e2 = a + 2 * (a - b) - 8;  // second-order term < 1/256
+            bool ok = kk * half * half + cmax < two63 &&
+                      2 * kk * half * H + (kk * half * half + cmax) / ((u128)1 << S) + 2 < two63 &&
+                      (cabs >> (2 * S)) < (two63 >> 1) && (cabs >> a) < ((u128)1 << 62) &&
+                      (e2 >= 127 || cabs < ((u128)1 << e2));
+            // digit bounds: m >= 2 from norm_bal(rem), rem in (-r/100, 2.01 r);
+            // digit 0 from norm_bal(d_0 - C); digit 1 gets digit 0's carry
+            u128 q2, ex2, q0, ex0;
+            norm_bounds(3 * (u128)r, r, fp, &q2, &ex2);
+            norm_bounds(X + cmax, r, fp, &q0, &ex0);
+            ok = ok && ex0 <= fp.delta && ex2 + q0 <= fp.delta;
+            c.p3_ok = ok ? 1 : 0;
+        }
     } else {
         c.s = 0;
         c.stages_per_norm = 0;

@@ -69,17 +69,125 @@ GFP_D u64 column_quot(i64 LL, i64 MID, i64 HH, const RadixConsts &rc, u64 &rem)
 //   q = T - (T >> (a - b)) - 2,  floor((c + B) / r) - q in [0, 3],
 // so rem = (c + B) - q r (= low 64 bits minus two shifts) is in [0, 4r)
 // without a 64 x 64 multiply.  Returns the signed carry q - 2^62.
-template <int S>
+// SPARSE == 3: a, b are compile-time (P2Radix<KD>); B mod 2^64 = 0 then.
+template <int S, int SPARSE = 2, int KD = 0>
 GFP_D i64 column_quot_p2(i64 LL, i64 MID, i64 HH, const RadixConsts &rc, u64 &rem)
 {
     const i64 mid = MID + (LL >> S);                // floor(c / 2^S)
     const i64 t2s = HH + (mid >> S);                 // floor(c / 2^(2S))
+    if constexpr (SPARSE == 3) {
+        constexpr int a = P2Radix<KD>::a, b = P2Radix<KD>::b;
+        static_assert(a >= 2 * S && a - 2 * S < 32 && 62 + b - a >= 0, "P2Radix vs S");
+        constexpr u64 bias_t = (1ULL << 62) + (1ULL << (62 + b - a));
+        const u64 T = (u64)(t2s >> (a - 2 * S)) + bias_t;
+        const u64 q = T - (T >> (a - b)) - 2;
+        // (2^62 r) mod 2^64 = 0 for a, b >= 2
+        const u64 clo = (u64)LL + ((u64)MID << S) + ((u64)HH << (2 * S));
+        rem = clo - (q << a) - (q << b);
+        return (i64)(q - (1ULL << 62));
+    }
     const u64 T = (u64)(t2s >> (rc.p2_sh & 31)) + rc.p2_bias_t;
     const u64 q = T - (T >> (rc.p2_ab & 63)) - 2;
     const u64 clo = (u64)LL + ((u64)MID << S) + ((u64)HH << (2 * S)) + rc.p2_bias_lo;
     rem = clo - (q << (rc.sp_a & 63)) - (q << (rc.p2_b & 63));
     return (i64)(q - (1ULL << 62));
 }
+
+// Mode 3 quotient (compile-time r = 2^a + 2^b, P2Radix<KD>), signed: no
+// bias.  With T = floor(c / 2^a) (arithmetic shifts of the sub-columns),
+//   q = T - floor(T 2^(b-a)) - 1,   c / r - q in (-0.01, 2.01),
+// (the second-order term c 2^(2(b-a) - a) is below 1/256 for the paper's
+// radices), so rem = c - q r (low 64 bits minus two shifts) lies in
+// (-r/100, 2.01 r) and q is the signed carry.
+template <int S, int KD>
+GFP_D i64 column_quot_p3(i64 LL, i64 MID, i64 HH, u64 &rem)
+{
+    constexpr int a = P2Radix<KD>::a, b = P2Radix<KD>::b;
+    static_assert(a >= 2 * S && a - 2 * S < 32, "P2Radix vs S");
+    const i64 mid = MID + (LL >> S);   // floor(c / 2^S) - HH 2^S
+    const i64 t2s = HH + (mid >> S);   // floor(c / 2^(2S))
+    const i64 T = t2s >> (a - 2 * S);  // floor(c / 2^a)
+    const i64 q = T - (T >> (a - b)) - 1;
+    const u64 clo = (u64)LL + ((u64)MID << S) + ((u64)HH << (2 * S));
+    rem = clo - ((u64)q << a) - ((u64)q << b);
+    return q;
+}
+
+// The carry rounds of one product, column by column (m = 0 .. k-1), shared
+// by the multiply kernels.  Column m's value is c_m = HH 2^(2S) + MID 2^S + LL.
+//   modes 0-2:  c_m = q_m r + d_m (column_quot*, d_m in [0, 4r)), then
+//               d_m + q_{m-1} = q2_m r + d2_m (norm_bal), digit = d2_m + q2_{m-1}
+//   mode 3, k <= 8 (SEQ): sequential carry: c_m + C_{m-1} = q_m r + rem_m,
+//               rem_m = q2_m r + d_m (norm_bal), digit = d_m, C_m = q_m + q2_m
+//               (one carry round less; for k >= 16 the serial chain across a
+//               block of columns costs more than it saves -- measured: the
+//               window multiplies keep the two-round form)
+// with the r^k = -1 wrap at m = 0 resolved by finish() (digits 0 and 1).
+template <int S, int SPARSE, int KD>
+struct ColReduce {
+    static constexpr bool SEQ = SPARSE == 3 && KD <= 8;
+    i64 q_prev = 0, d0 = 0, f1 = 0;
+    int q2_prev = 0;
+    // returns true when digit m (>= 2) is final in `out`
+    GFP_D bool column(int m, i64 LL, i64 MID, i64 HH, const RadixConsts &rc, i64 &out)
+    {
+        if constexpr (SEQ) {
+            u64 rem;
+            const i64 q = column_quot_p3<S, KD>(LL + q_prev, MID, HH, rem);
+            i64 d;
+            const int q2 = norm_bal<3, KD>((i64)rem, rc, d);
+            q_prev = q + q2;
+            if (m == 0) {
+                d0 = d;
+                return false;
+            }
+            if (m == 1) {
+                f1 = d;
+                return false;
+            }
+            out = d;
+            return true;
+        } else {
+            u64 rem;
+            i64 carry;
+            if (SPARSE >= 2) {
+                carry = column_quot_p2<S, SPARSE, KD>(LL, MID, HH, rc, rem);
+            } else {
+                const u64 qq = column_quot<S>(LL, MID, HH, rc, rem);
+                carry = (i64)(qq - (1ULL << 63));
+            }
+            bool fin = false;
+            if (m == 0) {
+                d0 = (i64)rem;
+            } else {
+                i64 d2;
+                const int q2 = norm_bal<SPARSE, KD>((i64)rem + q_prev, rc, d2);
+                if (m == 1) {
+                    f1 = d2;
+                } else {
+                    out = d2 + q2_prev;
+                    fin = true;
+                }
+                q2_prev = q2;
+            }
+            q_prev = carry;
+            return fin;
+        }
+    }
+    // digits 0 and 1 after the last column (the wrapped carry enters digit 0
+    // negated)
+    GFP_D void finish(const RadixConsts &rc, i64 &o0, i64 &o1)
+    {
+        i64 d2_0;
+        const int q2_0 = norm_bal<SPARSE, KD>(d0 - q_prev, rc, d2_0);
+        if constexpr (SEQ) {
+            o0 = d2_0;
+        } else {
+            o0 = d2_0 - q2_prev;
+        }
+        o1 = f1 + q2_0;
+    }
+};
 
 // x * y mod p for balanced lazy digits (|digit| <= r/2 + delta), output
 // balanced lazy digits.  Limbs are balanced too, x = xh 2^S + xl with
@@ -112,8 +220,7 @@ GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&
     //   round 3  f_m = d2_m + q2_{m-1}
     // with the r^k = -1 wrap at m = 0 (q_{-1} = -q_{k-1}).  Only column 0's
     // remainder and digit 1's pending carry wait for the last column.
-    i64 q_prev = 0, d0 = 0, f1 = 0;
-    int q2_prev = 0;
+    ColReduce<S, SPARSE, KD> cr;
 #pragma unroll
     for (int m = 0; m < KD; m++) {
         i64 LL = 0, SS = 0, HH = 0, LLn = 0, SSn = 0, HHn = 0;
@@ -149,41 +256,22 @@ GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&
         LL -= LLn;
         HH -= HHn;
         const i64 MID = KARA ? (SS - SSn) - LL - HH : SS - SSn;
-        u64 rem;
-        i64 carry;
-        if (SPARSE == 2) {
-            carry = column_quot_p2<S>(LL, MID, HH, rc, rem);
-        } else {
-            const u64 qq = column_quot<S>(LL, MID, HH, rc, rem);
-            carry = (i64)(qq - (1ULL << 63));
-        }
-        if (m == 0) {
-            d0 = (i64)rem;
-        } else {
-            i64 d2;
-            const int q2 = norm_bal<SPARSE>((i64)rem + q_prev, rc, d2);
-            if (m == 1)
-                f1 = d2;  // + q2_0, known only after the last column
+        i64 v;
+        if (cr.column(m, LL, MID, HH, rc, v)) {
+            if (STORE)
+                dst[m] = v;
             else
-            {
-                const i64 v = d2 + q2_prev;
-                if (STORE)
-                    dst[m] = v;
-                else
-                    f[m] = v;
-            }
-            q2_prev = q2;
+                f[m] = v;
         }
-        q_prev = carry;
     }
-    i64 d2_0;
-    const int q2_0 = norm_bal<SPARSE>(d0 - q_prev, rc, d2_0);
+    i64 o0, o1;
+    cr.finish(rc, o0, o1);
     if (STORE) {
-        dst[0] = d2_0 - q2_prev;
-        dst[1] = f1 + q2_0;
+        dst[0] = o0;
+        dst[1] = o1;
     } else {
-        f[0] = d2_0 - q2_prev;
-        f[1] = f1 + q2_0;
+        f[0] = o0;
+        f[1] = o1;
     }
 }
 
@@ -260,8 +348,7 @@ GFP_D void fast_mul_window_store(const i64 (&x)[KD], unsigned negx, const int2 *
         xl[i] = l0 * sg;
         xs[i] = xl[i] + xh[i];
     }
-    i64 q_prev = 0, d0 = 0, f1 = 0;
-    int q2_prev = 0;
+    ColReduce<S, SPARSE, KD> cr;
     // fully unrolled up to k = 16 (compile-time window addresses and wrap
     // signs); k = 32 keeps the block loop to bound the code size
     constexpr int UNR = KD <= 16 ? KD / 4 : 1;
@@ -298,32 +385,11 @@ GFP_D void fast_mul_window_store(const i64 (&x)[KD], unsigned negx, const int2 *
         }
 #pragma unroll
         for (int c = 0; c < 4; c++) {
-            const int m = m0 + c;
             const i64 MID = SS[c] - LL[c] - HH[c];
-            u64 rem;
-            i64 carry;
-            if (SPARSE == 2) {
-                carry = column_quot_p2<S>(LL[c], MID, HH[c], rc, rem);
-            } else {
-                const u64 qq = column_quot<S>(LL[c], MID, HH[c], rc, rem);
-                carry = (i64)(qq - (1ULL << 63));
-            }
-            if (m == 0) {
-                d0 = (i64)rem;
-            } else {
-                i64 d2;
-                const int q2 = norm_bal<SPARSE>((i64)rem + q_prev, rc, d2);
-                if (m == 1)
-                    f1 = d2;
-                else
-                    dst[m] = d2 + q2_prev;
-                q2_prev = q2;
-            }
-            q_prev = carry;
+            i64 v;
+            if (cr.column(m0 + c, LL[c], MID, HH[c], rc, v))
+                dst[m0 + c] = v;
         }
     }
-    i64 d2_0;
-    const int q2_0 = norm_bal<SPARSE>(d0 - q_prev, rc, d2_0);
-    dst[0] = d2_0 - q2_prev;
-    dst[1] = f1 + q2_0;
+    cr.finish(rc, dst[0], dst[1]);
 }

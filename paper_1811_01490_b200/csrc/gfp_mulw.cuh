@@ -65,8 +65,7 @@ __global__ void __launch_bounds__(128, 3)
             }
         }
         // ---- column blocks; carry rounds as in fast_mul_limbs
-        i64 q_prev = 0, d0 = 0, f1 = 0;
-        int q2_prev = 0;
+        ColReduce<S, SPARSE, KD> cr;
 #pragma unroll 1
         for (int m0 = 0; m0 < KD; m0 += 4) {
             i64 LL[4], SS[4], HH[4];
@@ -99,38 +98,15 @@ __global__ void __launch_bounds__(128, 3)
             }
 #pragma unroll
             for (int c = 0; c < 4; c++) {
-                const int m = m0 + c;
                 const i64 MID = SS[c] - LL[c] - HH[c];
-                u64 rem;
-                i64 carry;
-                if (SPARSE == 2) {
-                    carry = column_quot_p2<S>(LL[c], MID, HH[c], rc, rem);
-                } else {
-                    const u64 qq = column_quot<S>(LL[c], MID, HH[c], rc, rem);
-                    carry = (i64)(qq - (1ULL << 63));
-                }
-                if (m == 0) {
-                    d0 = (i64)rem;
-                } else {
-                    i64 d2;
-                    const int q2 = norm_bal<SPARSE>((i64)rem + q_prev, rc, d2);
-                    if (m == 1)
-                        f1 = d2;
-                    else
-                        z[m * n + e] = (u64)(d2 + q2_prev);  // lazy digit, scratch
-                    q2_prev = q2;
-                }
-                q_prev = carry;
+                i64 v;
+                if (cr.column(m0 + c, LL[c], MID, HH[c], rc, v))
+                    z[(m0 + c) * n + e] = (u64)v;  // lazy digit, scratch
             }
         }
         // ---- wrap carries into digits 0, 1; canonicalise
         i64 f[KD];
-        {
-            i64 d2_0;
-            const int q2_0 = norm_bal<SPARSE>(d0 - q_prev, rc, d2_0);
-            f[0] = d2_0 - q2_prev;
-            f[1] = f1 + q2_0;
-        }
+        cr.finish(rc, f[0], f[1]);
 #pragma unroll
         for (int d = 2; d < KD; d++)
             f[d] = (i64)z[d * n + e];
@@ -165,13 +141,17 @@ static inline int launch_mul_wide(int k, const u64 *x, const u64 *y, int64_t y_i
                              (int)smem);
         cudaFuncSetAttribute(k_mul_wide<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
+        cudaFuncSetAttribute(k_mul_wide<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
         attr = true;
     }
     int64_t blocks = (n + nt - 1) / nt;
     const int64_t cap = (int64_t)num_sms() * 3 * 8;
     if (blocks > cap)
         blocks = cap;
-    if (rc.p2_ok)
+    if (rc.p3_ok)
+        k_mul_wide<32, 3><<<(unsigned)blocks, nt, smem, st>>>(x, y, y_inc, z, n, rc);
+    else if (rc.p2_ok)
         k_mul_wide<32, 2><<<(unsigned)blocks, nt, smem, st>>>(x, y, y_inc, z, n, rc);
     else if (rc.sp_on)
         k_mul_wide<32, 1><<<(unsigned)blocks, nt, smem, st>>>(x, y, y_inc, z, n, rc);

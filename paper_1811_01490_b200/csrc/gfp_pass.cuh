@@ -45,7 +45,7 @@ template <int KD, int SPARSE>
 GFP_D void normalize_lane(i64 &v, int d, const RadixConsts &rc)
 {
     i64 rem;
-    int q = norm_bal<SPARSE>(v, rc, rem);
+    int q = norm_bal<SPARSE, KD>(v, rc, rem);
     int qin = __shfl_sync(FULL_MASK, q, (d - 1) & (KD - 1), KD);
     v = rem + (d == 0 ? -qin : qin);
 }
@@ -309,6 +309,10 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)pass_smem<KD>(256 / KD));
         }
+        if constexpr (P2Radix<KD>::a != 0)
+            cudaFuncSetAttribute((const void *)k_pass<KD, 3>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)pass_smem<KD>(256 / KD));
         attr_set = true;
     }
     PassArgs A;
@@ -365,6 +369,12 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
     if (A.in_em || A.out_em || A.ft_lh)
         return GFP_EUNSUPPORTED;
     dim3 grid((unsigned)((p->M + G - 1) / G), (unsigned)(in2 ? 2 * batch : batch));
+    if constexpr (P2Radix<KD>::a != 0) {
+        if (p->rc.p3_ok) {
+            launch_pdl(k_pass<KD, 3>, grid, threads, st, A, smem);
+            return cuda_status();
+        }
+    }
     if (p->rc.p2_ok) {
         launch_pdl(k_pass<KD, 2>, grid, threads, st, A, smem);
     } else if (p->rc.sp_on) {

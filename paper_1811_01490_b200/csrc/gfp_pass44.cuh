@@ -126,7 +126,7 @@ GFP_D void normalize_el(i64 (&v)[KD], const RadixConsts &rc)
     i64 rem[KD];
 #pragma unroll
     for (int d = 0; d < KD; d++)
-        q[d] = norm_bal<SPARSE>(v[d], rc, rem[d]);
+        q[d] = norm_bal<SPARSE, KD>(v[d], rc, rem[d]);
     v[0] = rem[0] - q[KD - 1];
 #pragma unroll
     for (int d = 1; d < KD; d++)
@@ -239,46 +239,66 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
             }
             if (A.in_canon)  // pass 0 only, where a = 0
                 to_balanced<KD>(x, rc.r);
-            if (pre) {  // pass 0 only (a = b = 0): pointwise product
-                i64 y[KD];
-#pragma unroll
-                for (int d = 0; d < KD; d++)
-                    y[d] = (i64)__ldg(pre + ((int64_t)d << lN) + pos);
-                fast_mul_lazy<KD, SPARSE>(x, y, x, rc);
-            }
         }
         // element t parks in slot t: holding four elements in registers
         // across the multiplies would cost occupancy
         i64 *slot = sm + (t * 32 + lane) * SLOT;
-        // the multiply is warp-uniform: lanes whose twiddle is a pure power
-        // of r (b = 0) multiply by table[0] = 1 instead of diverging; it
-        // stores each product digit to the slot as soon as it is final
-        bool parked = false;
-        if (__any_sync(FULL_MASK, active && (b || A.scale))) {
-            if (active) {
-                u64 ylh[KD];
-                const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(
-                    (A.ft_lh ? A.ft_lh : A.table_lh) + b * KD);
+        // Up to two multiplies through ONE inlined copy of the multiply (the
+        // kernel's code size matters: ~2/3 of it would be multiplies): the
+        // pointwise product by `pre` (pass 0 only, a = b = 0), then the
+        // twiddle omega^b.  The twiddle multiply is warp-uniform: lanes whose
+        // twiddle is a pure power of r (b = 0) multiply by table[0] = 1
+        // instead of diverging.  Each product digit is stored to the slot as
+        // soon as it is final; a second multiply reloads it.
+        const bool mul_tw = __any_sync(FULL_MASK, active && (b || A.scale));
+        const int nmul = (pre ? 1 : 0) + (mul_tw ? 1 : 0);
+#pragma unroll 1
+        for (int mi = 0; mi < nmul; mi++) {
+            const bool use_pre = pre && mi == 0;
+            if (mi > 0) {  // own slot: no cross-lane ordering needed
 #pragma unroll
                 for (int d = 0; d < KD; d += 2) {
-                    const ulonglong2 v = __ldg(tp + d / 2);
-                    ylh[d] = v.x;
-                    ylh[d + 1] = v.y;
+                    const longlong2 v = *reinterpret_cast<const longlong2 *>(slot + d);
+                    x[d] = v.x;
+                    x[d + 1] = v.y;
                 }
-                fast_mul_lazy_ylimbs<KD, SPARSE, true>(x, ylh, f, rc, negx, slot);
-                parked = true;
             }
-        } else if (active) {
+            if (active) {
+                u64 ylh[KD];
+                if (use_pre) {
+                    constexpr int S = FastSplit<KD>::S;
+#pragma unroll
+                    for (int d = 0; d < KD; d++) {
+                        int l, h;
+                        split_limbs<S>((i64)__ldg(pre + ((int64_t)d << lN) + pos), l, h);
+                        ylh[d] = (u64)(unsigned)l | ((u64)(unsigned)h << 32);
+                    }
+                } else {
+                    const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(
+                        (A.ft_lh ? A.ft_lh : A.table_lh) + b * KD);
+#pragma unroll
+                    for (int d = 0; d < KD; d += 2) {
+                        const ulonglong2 v = __ldg(tp + d / 2);
+                        ylh[d] = v.x;
+                        ylh[d + 1] = v.y;
+                    }
+                }
+                fast_mul_lazy_ylimbs<KD, SPARSE, true>(x, ylh, f, rc, use_pre ? 0u : negx, slot);
+            }
+        }
+        if (!mul_tw || !active) {
+            // no twiddle multiply: r^a alone (a digit renaming) or an idle lane
+            if (pre && active) {  // own slot (divergent: no warp barrier here)
+#pragma unroll
+                for (int d = 0; d < KD; d += 2) {
+                    const longlong2 v = *reinterpret_cast<const longlong2 *>(slot + d);
+                    x[d] = v.x;
+                    x[d + 1] = v.y;
+                }
+            }
 #pragma unroll
             for (int d = 0; d < KD; d++)
-                f[d] = ((negx >> d) & 1u) ? -x[d] : x[d];
-        }
-        if (!active) {
-#pragma unroll
-            for (int d = 0; d < KD; d++)
-                f[d] = 0;
-        }
-        if (!parked) {
+                f[d] = !active ? 0 : ((negx >> d) & 1u) ? -x[d] : x[d];
 #pragma unroll
             for (int d = 0; d < KD; d += 2)
                 *reinterpret_cast<longlong2 *>(slot + d) = make_longlong2(f[d], f[d + 1]);
@@ -332,6 +352,21 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
     case 2: p44::dft4<KD, INV, 2>(e[0], e[1], e[2], e[3]); break;
     default: p44::dft4<KD, INV, 3>(e[0], e[1], e[2], e[3]); break;
     }
+    // one balanced normalisation per output, then (last pass) the canonical
+    // form, once for all three store paths below (keeps the kernel's code
+    // small: the store paths only move digits)
+    const bool canon = A.canon || em_out;
+#pragma unroll
+    for (int u1 = 0; u1 < 4; u1++) {
+        p44::normalize_el<KD, SPARSE>(e[u1], rc);
+        if (canon) {
+            u64 c[KD];
+            lazy_to_canonical_bf<KD>(e[u1], c, rc);
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                e[u1][d] = (i64)c[d];
+        }
+    }
     if (em_out) {
         // last pass (Ns = M: output u of group j at j + u M), element-major,
         // possibly mapped host memory: park the canonical outputs in this
@@ -340,13 +375,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
         const int64_t j0 = (int64_t)blockIdx.x << 5;
 #pragma unroll
         for (int u1 = 0; u1 < 4; u1++) {
-            p44::normalize_el<KD, SPARSE>(e[u1], rc);
-            u64 c[KD];
-            lazy_to_canonical(e[u1], c, KD, rc);
             i64 *slot = sm + ((4 * w + u1) * 32 + lane) * SLOT;
 #pragma unroll
             for (int d = 0; d < KD; d += 2)
-                *reinterpret_cast<longlong2 *>(slot + d) = make_longlong2(c[d], c[d + 1]);
+                *reinterpret_cast<longlong2 *>(slot + d) = make_longlong2(e[u1][d], e[u1][d + 1]);
         }
         __syncwarp();
 #pragma unroll
@@ -376,19 +408,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
         asm volatile("bar.sync 1, 128;" ::: "memory");  // stage-2 slot reads done
 #pragma unroll
         for (int u1 = 0; u1 < 4; u1++) {
-            p44::normalize_el<KD, SPARSE>(e[u1], rc);
             const int u = w + 4 * u1;
-            if (A.canon) {
-                u64 c[KD];
-                lazy_to_canonical(e[u1], c, KD, rc);
 #pragma unroll
-                for (int d = 0; d < KD; d++)
-                    park[(d * 32 + lane) * 17 + u] = (i64)c[d];
-            } else {
-#pragma unroll
-                for (int d = 0; d < KD; d++)
-                    park[(d * 32 + lane) * 17 + u] = e[u1][d];
-            }
+            for (int d = 0; d < KD; d++)
+                park[(d * 32 + lane) * 17 + u] = e[u1][d];
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const int tid = threadIdx.x;  // < 128: the four stage-2 warps
@@ -411,21 +434,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
     const int64_t base = ((j >> lNs) << (lNs + 4)) + (j & nsmask);
 #pragma unroll
     for (int u1 = 0; u1 < 4; u1++) {
-        p44::normalize_el<KD, SPARSE>(e[u1], rc);
         const int64_t pos = base + ((int64_t)(w + 4 * u1) << lNs);
-        if (A.canon) {
-            u64 c[KD];
-            lazy_to_canonical(e[u1], c, KD, rc);
-            {
 #pragma unroll
-                for (int d = 0; d < KD; d++)
-                    __stcs(out + ((int64_t)d << lN) + pos, c[d]);
-            }
-        } else {
-#pragma unroll
-            for (int d = 0; d < KD; d++)
-                __stcs(out + ((int64_t)d << lN) + pos, (u64)e[u1][d]);
-        }
+        for (int d = 0; d < KD; d++)
+            __stcs(out + ((int64_t)d << lN) + pos, (u64)e[u1][d]);
     }
 }
 
@@ -497,7 +509,13 @@ static int launch_pass44(const PassArgs &A, int64_t M, int64_t nsets, cudaStream
     default: launch_pdl(k_pass44<KD, SP, IV, 16>, grid, 512, st, A); break;                   \
     }
         // mode 2 (shift quotients) for r = 2^a + 2^b, else the generic mode
-        if (A.rc.p2_ok) {
+        if (A.rc.p3_ok) {
+            if (inv) {
+                P44_LAUNCH(3, true)
+            } else {
+                P44_LAUNCH(3, false)
+            }
+        } else if (A.rc.p2_ok) {
             if (inv) {
                 P44_LAUNCH(2, true)
             } else {

@@ -17,6 +17,7 @@ Outputs (all under tests/golden/):
   elementwise_k{k}.npz   add/sub/mul/shift vectors per (k, r) config
   fft_small.npz          k=8 K=16 e=2 (N=256) forward + inverse vectors
   c1.npz                 C1: seed 0, k=8, N=4096 input and forward output
+  fft256_{in,fwd}.gfpv   GFPV files from the reference's write_gfpv (CLI interop)
   golden.json            roots, base-case op lists, digests of the large
                          configs (C2..C5), element-major sha256 prefixes
 """
@@ -163,6 +164,20 @@ def task_fft_small(_):
                          "count": 3}
 
 
+def task_gfpv(_):
+    """GFPV files written by the reference's own bench_cli.write_gfpv
+    (bench_cli.py:88-97): a seed-0 k=8 K=16 e=2 input (the bench-fft input
+    convention, bench_cli.py:383-394) and its forward transform -- the
+    byte-level interop fixture for the CLI's `fft` command."""
+    params, field, plan = field_plan(8, 256)
+    v = draws(params, 0, 256)
+    w = fft.dft_general(list(v), plan, field)
+    bench_cli.write_gfpv(os.path.join(HERE, "fft256_in.gfpv"), 8, params.r, v)
+    bench_cli.write_gfpv(os.path.join(HERE, "fft256_fwd.gfpv"), 8, params.r, w)
+    return "gfpv", {"k": 8, "K": 16, "e": 2, "N": 256, "seed": 0,
+                    "in": digest(v), "fwd": digest(w)}
+
+
 def task_c1(_):
     params, field, plan = field_plan(8, 4096)
     v = draws(params, 0, 4096)
@@ -280,7 +295,7 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--jobs", type=int, default=os.cpu_count())
     args = ap.parse_args()
-    tasks = [(task_ops, None), (task_fft_small, None), (task_c1, None),
+    tasks = [(task_ops, None), (task_fft_small, None), (task_gfpv, None), (task_c1, None),
              (task_c2, None), (task_c4_prefix, None), (task_c5, None)]
     tasks += [(task_elementwise, c) for c in ELEMENTWISE_CONFIGS]
     roots = [(8, 256), (8, 4096), (8, 1 << 16), (8, 1 << 24), (16, 1 << 10),

@@ -78,6 +78,18 @@ def full(path):
         for m in FULL_METRICS:
             if m in d:
                 print("  %-60s %s" % (m, d[m]))
+        # warp-state breakdown (stall reasons, cycles per issued instruction)
+        st = []
+        for m, v in d.items():
+            if m.startswith("smsp__average_warp_latency_issue_stalled_") or (
+                    m.startswith("smsp__average_warps_issue_stalled_") and m.endswith("_per_issue_active.ratio")):
+                try:
+                    st.append((float(v.replace(",", "")), m))
+                except ValueError:
+                    pass
+        for v, m in sorted(st, reverse=True)[:12]:
+            if v > 0.01:
+                print("  stall %-70s %s" % (m, v))
 
 
 if __name__ == "__main__":
