@@ -122,6 +122,28 @@ GFP_D void dft4(i64 (&x0)[KD], i64 (&x1)[KD], i64 (&x2)[KD], i64 (&x3)[KD])
 template <int KD, int SPARSE>
 GFP_D void normalize_el(i64 (&v)[KD], const RadixConsts &rc)
 {
+    if constexpr (SPARSE == 3) {
+        // compile-time r = 2^a + 2^b: digit d becomes
+        //   ((v_d + 2^(a-1)) mod 2^a) - 2^(a-1) + (q_{d-1} - q_d 2^b)
+        // with the small correction q_{d-1} - q_d 2^b formed in 32 bits (one
+        // IMAD) and added once (|q| <= 2^5, so it fits easily)
+        constexpr int a = P2Radix<KD>::a, b = P2Radix<KD>::b;
+        constexpr i64 half = (i64)1 << (a - 1), mask = ((i64)1 << a) - 1;
+        int q[KD];
+        i64 m[KD];
+#pragma unroll
+        for (int d = 0; d < KD; d++) {
+            const i64 vb = v[d] + half;
+            q[d] = (int)(vb >> a);
+            m[d] = vb & mask;
+        }
+#pragma unroll
+        for (int d = 0; d < KD; d++) {
+            const int cin = d ? q[d - 1] : -q[KD - 1];
+            v[d] = m[d] - half + (i64)(cin - (q[d] << b));
+        }
+        return;
+    }
     int q[KD];
     i64 rem[KD];
 #pragma unroll
@@ -177,6 +199,29 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
     // ---- phase A: load + twiddle elements t = w + NW i (16 / NW per thread)
+    // With two or more elements per thread the digit-major loads of element
+    // i + 1 are issued (cp.async, 8 B per digit row, coalesced across the
+    // warp) into this warp's staging rows while element i is multiplied, so
+    // the HBM latency hides behind the multiply (was ~20% of the stall
+    // samples); the rotation r^a is applied when the row is read back.
+    extern __shared__ __align__(16) u64 pf_stage[];  // [NW][KD][32]
+    const bool pf = NW <= 8 && !em_in;
+    u64 *stg = pf_stage + w * (KD * 32) + lane;
+    auto prefetch = [&](int i) {
+        if (active) {
+            const u64 *src = in + j + ((int64_t)(w + NW * i) << lM);
+#pragma unroll
+            for (int r_ = 0; r_ < KD; r_++) {
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(stg + r_ * 32);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa),
+                             "l"(src + ((int64_t)r_ << lN))
+                             : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (pf)
+        prefetch(0);
     i64 e[4][KD];
 #pragma unroll 1
     for (int i = 0; i < 16 / NW; i++) {
@@ -229,6 +274,13 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
                     x[d] = v.x;
                     x[d + 1] = v.y;
                 }
+            } else if (pf) {
+                asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+                for (int d = 0; d < KD; d++)
+                    x[d] = (i64)stg[((d - tw.as) & (KD - 1)) * 32];
+                if (i + 1 < 16 / NW)  // own rows, already read: refill them
+                    prefetch(i + 1);
             } else {
                 // rows are N words apart; k N words fit 32-bit offsets (N <= 2^26)
                 const u64 *src = in + pos;
@@ -480,6 +532,20 @@ static inline void launch_pdl(void (*kern)(PassArgs), dim3 grid, int threads, cu
     cudaLaunchKernelEx(&cfg, kern, A);
 }
 
+// NW <= 8: dynamic shared memory for the cp.async staging rows ([NW][k][32])
+template <int KD, int SP, bool IV, int NW>
+static inline void launch_p44(dim3 grid, cudaStream_t st, const PassArgs &A)
+{
+    const size_t smem = (size_t)NW * KD * 32 * sizeof(u64);
+    static bool set = false;
+    if (!set) {
+        cudaFuncSetAttribute(k_pass44<KD, SP, IV, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        set = true;
+    }
+    launch_pdl(k_pass44<KD, SP, IV, NW>, grid, NW * 32, st, A, smem);
+}
+
 // launcher: returns 1 when it handled the pass
 template <int KD>
 static int launch_pass44(const PassArgs &A, int64_t M, int64_t nsets, cudaStream_t st)
@@ -504,8 +570,8 @@ static int launch_pass44(const PassArgs &A, int64_t M, int64_t nsets, cudaStream
         const bool inv = A.rot_inv != 0;
 #define P44_LAUNCH(SP, IV)                                                                    \
     switch (nw) {                                                                             \
-    case 4: launch_pdl(k_pass44<KD, SP, IV, 4>, grid, 128, st, A); break;                     \
-    case 8: launch_pdl(k_pass44<KD, SP, IV, 8>, grid, 256, st, A); break;                     \
+    case 4: launch_p44<KD, SP, IV, 4>(grid, st, A); break;                                     \
+    case 8: launch_p44<KD, SP, IV, 8>(grid, st, A); break;                                     \
     default: launch_pdl(k_pass44<KD, SP, IV, 16>, grid, 512, st, A); break;                   \
     }
         // mode 2 (shift quotients) for r = 2^a + 2^b, else the generic mode
