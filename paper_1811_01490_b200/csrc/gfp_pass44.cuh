@@ -33,7 +33,11 @@
 #include "gfp_fast.cuh"
 
 #ifndef P44_MINB
-#define P44_MINB 4  // CTAs per SM the NW = 4 variant is register-bounded for
+#define P44_MINB 5  // CTAs per SM the NW = 4 variant is register-bounded for (96 regs)
+#endif
+#ifndef P44_PF_MINNW
+#define P44_PF_MINNW 8  // smallest NW that stages the next element with cp.async (NW = 4
+                        // keeps 40 KB smem for 5 CTAs / SM: measured 1.5% faster on C4)
 #endif
 
 namespace p44 {
@@ -205,7 +209,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
     // the HBM latency hides behind the multiply (was ~20% of the stall
     // samples); the rotation r^a is applied when the row is read back.
     extern __shared__ __align__(16) u64 pf_stage[];  // [NW][KD][32]
-    const bool pf = NW <= 8 && !em_in;
+    constexpr bool PF = NW <= 8 && NW >= P44_PF_MINNW;
+    const bool pf = PF && !em_in;
     u64 *stg = pf_stage + w * (KD * 32) + lane;
     auto prefetch = [&](int i) {
         if (active) {
@@ -536,7 +541,7 @@ static inline void launch_pdl(void (*kern)(PassArgs), dim3 grid, int threads, cu
 template <int KD, int SP, bool IV, int NW>
 static inline void launch_p44(dim3 grid, cudaStream_t st, const PassArgs &A)
 {
-    const size_t smem = (size_t)NW * KD * 32 * sizeof(u64);
+    const size_t smem = NW >= P44_PF_MINNW ? (size_t)NW * KD * 32 * sizeof(u64) : 0;
     static bool set = false;
     if (!set) {
         cudaFuncSetAttribute(k_pass44<KD, SP, IV, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
