@@ -601,6 +601,37 @@ def extra_configs(args, dev, flush, stream):
             torch.cuda.empty_cache()
         except Exception as exc:
             res[key] = {"error": str(exc)[:300]}
+    # the word-prime transform (MontField over P1) and the
+    # cyclic convolution, 8 x 2^20 words; HBM roofline of the NTT passes
+    # (each radix-16 pass streams 2 x 8 bytes per word)
+    try:
+        q, n, B = gp.P1, 1 << 20, 8
+        ctx = gp.word_prime(q)
+        wplan = gp.conv_plan(ctx, n, False)
+        g = torch.Generator(device="cuda").manual_seed(11)
+        xw = (torch.randint(0, 1 << 62, (B, n), device="cuda", generator=g) % q).view(torch.uint64)
+        yw = (torch.randint(0, 1 << 62, (B, n), device="cuda", generator=g) % q).view(torch.uint64)
+        zw = torch.empty_like(xw)
+
+        def nstep():
+            gp.word_ntt(xw, wplan, out=zw)
+        t = timed_loop(nstep, steps, 2, 1, flush, stream)
+        ms = sum(t) / len(t)
+        npass = 5  # 2^20 = 16^5
+        gbs = npass * 2 * 8 * n * B / (ms * 1e-3) / 1e9
+        entry = {"workload": "word-prime NTT / cyclic convolution, q = P1, 8 x 2^20",
+                 "ms_ntt": ms, "ntt_words_per_s": B * n / (ms * 1e-3),
+                 "ntt_hbm_gbs": gbs}
+
+        def cstep():
+            gp.word_convolve(xw, yw, wplan, out=zw)
+        t = timed_loop(cstep, steps, 2, 1, flush, stream)
+        ms = sum(t) / len(t)
+        entry.update(ms_cyclic_convolution=ms, conv_words_per_s=B * n / (ms * 1e-3))
+        res["word"] = entry
+        del xw, yw, zw
+    except Exception as exc:
+        res["word"] = {"error": str(exc)[:300]}
     return res
 
 

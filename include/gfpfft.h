@@ -185,6 +185,47 @@ int64_t gfp_fft_plan_last_launches(const gfp_fft_plan *plan);
 int gfp_probe_imad_wide(int64_t iters, int blocks, int threads, float *ms_out, double *ops_out,
                         void *stream);
 
+/* ------------------------------------------------------------------------
+ * Word-prime transform: DFT over Z/qZ, q an odd prime < 2^63, on Montgomery
+ * residues (R = 2^64), and the convolutions built on it.  Replaces the
+ * reference's MontField transform (fft.py:376-421 with word_field.py:103-200)
+ * and cyclic_convolution / negacyclic_convolution (gfp_mult.py:230-386).
+ * Buffers are plain uint64[batch][n] device arrays of residues in [0, q).
+ * ------------------------------------------------------------------------ */
+typedef struct gfp_word_plan gfp_word_plan;
+
+/* WordPrime.make constants (word_field.py:111-119): -q^-1 mod 2^64,
+   2^128 mod q, 2^64 mod q.  GFP_EINVAL unless q is odd, 3 <= q < 2^63. */
+int gfp_word_consts(uint64_t q, uint64_t *qinv, uint64_t *r2, uint64_t *one);
+
+/* z[i] = mont_mul(a[i], b[i]) = a b 2^-64 mod q (word_field.py:133-140). */
+int gfp_word_vec_mont_mul(uint64_t q, const uint64_t *a, const uint64_t *b, uint64_t *z,
+                          int64_t n, void *stream);
+
+/* Plan for n-point transforms (n a power of two dividing q - 1) at the
+   Montgomery-form root omega: GFP_EINVAL unless omega^n = 1 and
+   omega^(n/2) = -1 (build_plan's check, fft.py:250-254).  negacyclic != 0:
+   theta is a primitive 2n-th root with theta^2 = omega and gfp_word_convolve
+   computes the product mod (X^n + 1) (_nega_plan, gfp_mult.py:280-305);
+   otherwise mod (X^n - 1) (_cyclic_plan, gfp_mult.py:308-322). */
+int gfp_word_plan_create(gfp_word_plan **plan, uint64_t q, int64_t n, uint64_t omega,
+                         int negacyclic, uint64_t theta, void *stream);
+int gfp_word_plan_destroy(gfp_word_plan *plan);
+
+/* Natural-order DFT of Montgomery residues (dft_general on a MontField plan,
+   fft.py:298-360); inverse != 0: at omega^-1 with the n^-1 scale
+   (dft_inverse, fft.py:363-370).  in may equal out. */
+int gfp_word_ntt_exec(gfp_word_plan *plan, const uint64_t *in, uint64_t *out, int64_t batch,
+                      int inverse, void *stream);
+
+/* Convolution of standard-form inputs in [0, q) (GFP_EINVAL otherwise:
+   _check_reduced, gfp_mult.py:361-366), standard-form output: _convolve
+   (gfp_mult.py:351-358) -- weights, two forward transforms, pointwise
+   product, inverse transform and the output weights with 1/n.  Synchronous
+   (the input range check). */
+int gfp_word_convolve(gfp_word_plan *plan, const uint64_t *x, const uint64_t *y, uint64_t *out,
+                      int64_t batch, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

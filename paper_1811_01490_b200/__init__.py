@@ -25,6 +25,10 @@ from .fft import (BASE_SIZES, FftPlan, build_plan, dft_base, dft_general,  # noq
                   dft_inverse, fft as fft_tensor, fft_host, poly_mul, poly_mul_host,
                   poly_mul_list, roots_for, stride_permutation, twiddle_apply)
 from . import vec  # noqa: E402
+from .word import (MontField, WordPlan, WordPrime, conv_plan,  # noqa: E402
+                   cyclic_convolution, mont_convert_in, mont_convert_out, mont_inv, mont_mul,
+                   negacyclic_convolution, word_convolve, word_ntt, word_pow, word_prime,
+                   word_primitive_root)
 
 DEFAULT_RADIX = {
     8: (1 << 59) + (1 << 16),
@@ -44,5 +48,8 @@ __all__ = [
     "P1", "P2", "BASE_SIZES", "FftPlan", "build_plan", "dft_base", "dft_general",
     "dft_inverse", "stride_permutation", "twiddle_apply", "fft_tensor", "fft_host",
     "poly_mul", "poly_mul_host", "poly_mul_list", "roots_for", "vec", "DEFAULT_RADIX",
+    "MontField", "WordPlan", "WordPrime", "conv_plan", "cyclic_convolution",
+    "negacyclic_convolution", "mont_convert_in", "mont_convert_out", "mont_inv", "mont_mul",
+    "word_convolve", "word_ntt", "word_pow", "word_prime", "word_primitive_root",
     "__version__",
 ]

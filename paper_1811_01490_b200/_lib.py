@@ -41,6 +41,13 @@ SIGNATURES = {
     "gfp_vec_uniform": (_int, [_u64p, _i64, _int, _u64, _u64, _vp]),
     "gfp_to_digit_major": (_int, [_u64p, _u64p, _i64, _int, _vp]),
     "gfp_to_element_major": (_int, [_u64p, _u64p, _i64, _int, _vp]),
+    "gfp_word_consts": (_int, [_u64, ctypes.POINTER(ctypes.c_uint64),
+                               ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]),
+    "gfp_word_vec_mont_mul": (_int, [_u64, _u64p, _u64p, _u64p, _i64, _vp]),
+    "gfp_word_plan_create": (_int, [ctypes.POINTER(_vp), _u64, _i64, _u64, _int, _u64, _vp]),
+    "gfp_word_plan_destroy": (_int, [_vp]),
+    "gfp_word_ntt_exec": (_int, [_vp, _u64p, _u64p, _i64, _int, _vp]),
+    "gfp_word_convolve": (_int, [_vp, _u64p, _u64p, _u64p, _i64, _vp]),
     "gfp_fft_plan_create": (_int, [ctypes.POINTER(_vp), _int, _u64, _int, _int,
                                    ctypes.POINTER(ctypes.c_uint64), _vp]),
     "gfp_fft_plan_destroy": (_int, [_vp]),

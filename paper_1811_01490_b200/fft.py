@@ -121,6 +121,9 @@ def build_plan(field, K, e, omega, cheap_twiddle=None, threads=1):
     primitive N-th root, K != 2k, or omega^(N/2k) is neither r nor 1/r --
     the reference's rejections, checked on the device.
     """
+    from .word import MontField, build_word_plan
+    if isinstance(field, MontField):  # the word-prime transform (csrc/gfp_word.cu)
+        return build_word_plan(field, K, e, omega)
     if K not in BASE_SIZES:
         raise ValueError("unsupported base-case size")
     if e < 1:
@@ -255,6 +258,9 @@ def dft_general(v, plan, field=None, profile=None):
     "transform" and "download" (the device fuses the reference's
     permutation / basecase / twiddle phases into one kernel per pass).
     """
+    from .word import WordPlan, dft_word
+    if isinstance(plan, WordPlan):
+        return dft_word(v, plan)
     if len(v) != plan.N:
         raise ValueError("vector length must equal K^e")
     _run_list(v, plan, False, profile)
@@ -263,6 +269,9 @@ def dft_general(v, plan, field=None, profile=None):
 
 def dft_inverse(v, plan, field=None, profile=None):
     """Inverse transform including the 1/N scale (fft.py:363-370)."""
+    from .word import WordPlan, dft_word
+    if isinstance(plan, WordPlan):
+        return dft_word(v, plan, inverse=True)
     if len(v) != plan.N:
         raise ValueError("vector length must equal K^e")
     _run_list(v, plan, True, profile)

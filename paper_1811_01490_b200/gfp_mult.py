@@ -39,6 +39,16 @@ class CrtParams:
     p1: int = P1
     p2: int = P2
 
+    @property
+    def p1_ctx(self):
+        from .word import word_prime
+        return word_prime(self.p1)
+
+    @property
+    def p2_ctx(self):
+        from .word import word_prime
+        return word_prime(self.p2)
+
     @classmethod
     def make(cls, q1=P1, q2=P2):
         from math import gcd

@@ -18,6 +18,7 @@ Outputs (all under tests/golden/):
   fft_small.npz          k=8 K=16 e=2 (N=256) forward + inverse vectors
   c1.npz                 C1: seed 0, k=8, N=4096 input and forward output
   fft256_{in,fwd}.gfpv   GFPV files from the reference's write_gfpv (CLI interop)
+  word.npz               word-prime transforms and cyclic / negacyclic convolutions
   golden.json            roots, base-case op lists, digests of the large
                          configs (C2..C5), element-major sha256 prefixes
 """
@@ -178,6 +179,50 @@ def task_gfpv(_):
                     "in": digest(v), "fwd": digest(w)}
 
 
+def task_word(_):
+    """The word-prime layer (word_field.py, fft.py MontField, gfp_mult.py
+    convolutions) over the default prime pair: dft_general / dft_inverse on
+    MontField plans at the reference's word_primitive_root, and
+    cyclic / negacyclic convolutions of seeded standard-form vectors."""
+    from gfpfft import word_field as W
+    from gfpfft.fft import MontField
+    out, meta = {}, {"transforms": [], "cyclic": [], "negacyclic": []}
+    rng = random.Random(0x3D)
+    for q in (W.P1, W.P2):
+        ctx = W.word_prime(q)
+        field = MontField(ctx)
+        for K, e in [(8, 1), (8, 2), (16, 2), (32, 2), (64, 2), (8, 3), (16, 3)]:
+            N = K ** e
+            om = W.word_primitive_root(ctx, N)
+            plan = fft.build_plan(field, K, e, om)
+            v = [rng.randrange(q) for _ in range(N)]
+            tag = "%d_%d_%d" % (q % 1000, K, e)
+            out["dft_in_" + tag] = np.array(v, dtype=np.uint64)
+            out["dft_fwd_" + tag] = np.array(fft.dft_general(list(v), plan, field), dtype=np.uint64)
+            out["dft_inv_" + tag] = np.array(fft.dft_inverse(list(v), plan, field), dtype=np.uint64)
+            meta["transforms"].append([q, K, e, om, tag])
+        for n in (1, 2, 4, 8, 64, 128, 256, 1024, 4096):
+            f = [rng.randrange(q) for _ in range(n)]
+            g = [rng.randrange(q) for _ in range(n)]
+            tag = "%d_%d" % (q % 1000, n)
+            out["cyc_f_" + tag] = np.array(f, dtype=np.uint64)
+            out["cyc_g_" + tag] = np.array(g, dtype=np.uint64)
+            out["cyc_h_" + tag] = np.array(gfp_mult.cyclic_convolution(f, g, ctx, n),
+                                           dtype=np.uint64)
+            meta["cyclic"].append([q, n, tag])
+        for k in (1, 2, 4, 8, 16, 32, 64, 128, 512):
+            x = [rng.randrange(q) for _ in range(k)]
+            y = [rng.randrange(q) for _ in range(k)]
+            tag = "%d_%d" % (q % 1000, k)
+            out["neg_x_" + tag] = np.array(x, dtype=np.uint64)
+            out["neg_y_" + tag] = np.array(y, dtype=np.uint64)
+            out["neg_h_" + tag] = np.array(gfp_mult.negacyclic_convolution(x, y, ctx, k),
+                                           dtype=np.uint64)
+            meta["negacyclic"].append([q, k, tag])
+    np.savez_compressed(os.path.join(HERE, "word.npz"), **out)
+    return "word", meta
+
+
 def task_c1(_):
     params, field, plan = field_plan(8, 4096)
     v = draws(params, 0, 4096)
@@ -295,7 +340,8 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--jobs", type=int, default=os.cpu_count())
     args = ap.parse_args()
-    tasks = [(task_ops, None), (task_fft_small, None), (task_gfpv, None), (task_c1, None),
+    tasks = [(task_ops, None), (task_fft_small, None), (task_gfpv, None), (task_word, None),
+             (task_c1, None),
              (task_c2, None), (task_c4_prefix, None), (task_c5, None)]
     tasks += [(task_elementwise, c) for c in ELEMENTWISE_CONFIGS]
     roots = [(8, 256), (8, 4096), (8, 1 << 16), (8, 1 << 24), (16, 1 << 10),
