@@ -333,6 +333,27 @@ def _verify_checks(k, r, seed, samples):
            "" if bad is None else "mul counterexample a=%d b=%d" % (A[bad], B[bad]),
            None if bad is None else (enc(A[bad]), enc(B[bad])))
 
+    # the word-prime layer (gfp_mult.negacyclic_convolution over the prime
+    # pair, bench_cli.py:185-194), on the device
+    ok, detail = True, ""
+    for ctx in (crt.p1_ctx, crt.p2_ctx):
+        for _ in range(max(1, samples // 8)):
+            xs = [rng.randrange(ctx.q) for _ in range(k)]
+            ys = [rng.randrange(ctx.q) for _ in range(k)]
+            want = [0] * k
+            for i in range(k):
+                for jj in range(k):
+                    if i + jj < k:
+                        want[i + jj] += xs[i] * ys[jj]
+                    else:
+                        want[i + jj - k] -= xs[i] * ys[jj]
+            if list(gp.negacyclic_convolution(xs, ys, ctx, k)) != [w % ctx.q for w in want]:
+                ok, detail = False, "negacyclic counterexample q=%d" % ctx.q
+                break
+        if not ok:
+            break
+    yield "negacyclic_vs_schoolbook", ok, detail
+
     K, e = 2 * k, 2
     N = K ** e
     _, field, plan = _plan_for(k, r, K, e)

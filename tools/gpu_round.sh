@@ -1,0 +1,16 @@
+# One B200 pass over everything the round reports: GPU parity suite, smoke,
+# default bench line, reference arm, the ncu launch list of the default bench
+# command, and ncu --set full summaries of the C2 / C4 pass kernels.
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"
+tail -2 gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?"
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench exit $?"
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref exit $?"
+CMD="python bench.py --steps 3 --warmup 3 --no-extra --no-cpu"
+$CMD > gpurun_out/plain.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu1.log 2>&1; echo "ncu1 exit $?"
+python tools/ncu_summary.py launches gpurun_out/launches.csv > gpurun_out/launches_summary.txt 2>&1
+bash tools/gpu_prof.sh c2 8 8 c2 k_pass 786432
+bash tools/gpu_prof.sh c4 7 1 c4 k_pass 16777216
