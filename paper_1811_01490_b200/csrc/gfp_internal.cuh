@@ -33,7 +33,8 @@ struct PassArgs {
     int64_t batch_stride;
     int64_t batch;
     int lN, lM, lNs;   // log2 of N, M = N/K and Ns (all powers of two)
-    int lG;            // log2 of the groups per CTA
+    int lG;            // log2 of the groups per CTA (k_pass)
+    int gpc;           // groups per CTA, 1..32 (k_pass44; 32 unless the grid is under two waves)
     int neg_exp;   // twiddle exponent N - E (inverse transform)
     int rot_inv;   // base-case root of this execution is 1/r (rotations by r^-t)
     int root_inv;  // the plan's omega^M is 1/r (twiddle split r^-a omega^b)

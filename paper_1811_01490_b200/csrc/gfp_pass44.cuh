@@ -193,8 +193,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
     u64 *out = out_base + bidx * A.batch_stride;
     const u64 *pre = A.pre ? A.pre + bidx * A.batch_stride : nullptr;
     const RadixConsts rc = A.rc;
-    const int64_t j = ((int64_t)blockIdx.x << 5) + lane;
-    const bool active = j < M;
+    // gpc consecutive groups per CTA (32, or fewer to spread a small grid
+    // over every SM: launch_pass44)
+    const int gpc = A.gpc;
+    const int64_t j0 = (int64_t)blockIdx.x * gpc;
+    const int64_t j = j0 + lane;
+    const bool active = lane < gpc && j < M;
 
     // programmatic dependent launch: let the next pass's CTAs be scheduled
     // as this grid drains, and wait for the previous pass's writes before the
@@ -240,13 +244,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
             // host memory: the warp's 32 elements (j0 .. j0 + 31, t) are 2 KB
             // contiguous; read them with lane-contiguous 16 B loads (full
             // 512 B requests over PCIe) into this row's smem slots
-            const int64_t j0 = (int64_t)blockIdx.x << 5;
             const u64 *rowp = em_in + (j0 + ((int64_t)t << lM)) * KD;
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 const int e = (lane >> 2) + 8 * q, dp = (lane & 3) * 2;
                 ulonglong2 v = make_ulonglong2(0, 0);
-                if (j0 + e < M && j0 + e + ((int64_t)t << lM) < n_in)
+                if (e < gpc && j0 + e < M && j0 + e + ((int64_t)t << lM) < n_in)
                     v = reinterpret_cast<const ulonglong2 *>(rowp)[lane + 32 * q];
                 *reinterpret_cast<ulonglong2 *>(sm + (t * 32 + e) * SLOT + dp) = v;
             }
@@ -429,7 +432,6 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
         // possibly mapped host memory: park the canonical outputs in this
         // warp's own stage-2 slots (rows 4 w + u1), then write each u's 32
         // elements (2 KB contiguous) with lane-contiguous 16 B stores
-        const int64_t j0 = (int64_t)blockIdx.x << 5;
 #pragma unroll
         for (int u1 = 0; u1 < 4; u1++) {
             i64 *slot = sm + ((4 * w + u1) * 32 + lane) * SLOT;
@@ -447,7 +449,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
                 const int e = (lane >> 2) + 8 * q, dp = (lane & 3) * 2;
                 const longlong2 v =
                     *reinterpret_cast<const longlong2 *>(sm + ((4 * w + u1) * 32 + e) * SLOT + dp);
-                if (j0 + e < M && ubase + e < A.n_out)
+                if (e < gpc && j0 + e < M && ubase + e < A.n_out)
                     reinterpret_cast<ulonglong2 *>(rowp)[lane + 32 * q] =
                         make_ulonglong2((u64)v.x, (u64)v.y);
             }
@@ -460,7 +462,6 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
         // outputs digit-major ([d][g][u], row pitch 17: conflict-free both
         // ways) over the slots, then write each digit row's 512 consecutive
         // positions lane-contiguously.
-        const int64_t j0 = (int64_t)blockIdx.x << 5;
         i64 *park = sm;
         asm volatile("bar.sync 1, 128;" ::: "memory");  // stage-2 slot reads done
 #pragma unroll
@@ -477,7 +478,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
         for (int q4 = 0; q4 < 4; q4++) {
             const int q = tid + 128 * q4;      // position 16 j0 + q
             const int g = q >> 4, u = q & 15;  // group j0 + g, output u
-            if (j0 + g < M) {
+            if (g < gpc && j0 + g < M) {
 #pragma unroll
                 for (int d = 0; d < KD; d++)
                     __stcs(obase + ((int64_t)d << lN) + q, (u64)park[(d * 32 + g) * 17 + u]);
@@ -553,15 +554,14 @@ static inline void launch_p44(dim3 grid, cudaStream_t st, const PassArgs &A)
 
 // launcher: returns 1 when it handled the pass
 template <int KD>
-static int launch_pass44(const PassArgs &A, int64_t M, int64_t nsets, cudaStream_t st)
+static int launch_pass44(const PassArgs &A0, int64_t M, int64_t nsets, cudaStream_t st)
 {
     if constexpr (KD != 8) {
         return 0;
     } else {
-        if (!pass44_enabled(KD, A.rc))
+        if (!pass44_enabled(KD, A0.rc))
             return 0;
         const int64_t ctas = ((M + 31) / 32) * nsets;
-        dim3 grid((unsigned)((M + 31) / 32), (unsigned)nsets);
         // elements per thread in phase A: 4 when the grid fills the GPU,
         // fewer (more warps per CTA) for small transforms (C1, C2)
         static int nw_env = -1;
@@ -572,6 +572,20 @@ static int launch_pass44(const PassArgs &A, int64_t M, int64_t nsets, cudaStream
         int nw = ctas >= 4 * (int64_t)num_sms() ? 4 : ctas >= (int64_t)num_sms() ? 8 : 16;
         if (nw_env == 4 || nw_env == 8 || nw_env == 16)
             nw = nw_env;
+        // groups per CTA: 32.  (Spreading a grid under two waves over every
+        // SM with fewer groups per CTA was measured: no gain for C1 / C2,
+        // whose passes are latency-bound per CTA; kept as an experiment hook.)
+        int gpc = 32;
+        static int gpc_env = -1;
+        if (gpc_env < 0) {
+            const char *e = getenv("GFP_PASS44_GPC");  // experiment hook
+            gpc_env = e ? atoi(e) : 0;
+        }
+        if (gpc_env >= 1 && gpc_env <= 32)
+            gpc = gpc_env;
+        PassArgs A = A0;
+        A.gpc = gpc;
+        dim3 grid((unsigned)((M + gpc - 1) / gpc), (unsigned)nsets);
         const bool inv = A.rot_inv != 0;
 #define P44_LAUNCH(SP, IV)                                                                    \
     switch (nw) {                                                                             \
