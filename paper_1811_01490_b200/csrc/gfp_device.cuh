@@ -57,6 +57,11 @@ struct RadixConsts {
     // mode 3: r is the paper's radix for k (P2Radix<k>, compile-time a, b) and
     // the sequential-carry bounds hold (ColReduce, gfp_fast.cuh)
     int p3_ok;
+    // -1, passed at run time: a window digit negated with it stays an opaque
+    // operand, so ptxas keeps its products as fused IMAD.WIDE (a literal
+    // negation is folded into the products, which then split into
+    // IMAD + IMAD.HI pairs: measured 360 extra instructions per k = 16 multiply)
+    int neg_one;
 };
 
 // ---------------------------------------------------------------------------

@@ -148,6 +148,7 @@ RadixConsts make_consts(int k, u64 r)
     c.bias_lo = (u64)bias;
     c.bias_hi = (u64)(bias >> 64);
     c.rinv = 1.0 / (double)r;
+    c.neg_one = -1;
     c.w = 64 - c.sh;
     if (c.w < 64) {
         u128 m = ((u128)1 << (64 + c.w)) / r;

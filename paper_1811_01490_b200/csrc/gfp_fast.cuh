@@ -378,8 +378,8 @@ GFP_D void fast_mul_window_store(const i64 (&x)[KD], unsigned negx, const int2 *
                     win[c] = win[c - 1];
                 const int j = m0 - i - 1;
                 int2 v = ywin[((j + KD) & (KD - 1)) * stride];
-                if (j < 0)
-                    v = make_int2(-v.x, -v.y);
+                if (j < 0)  // r^k = -1 (rc.neg_one: see RadixConsts)
+                    v = make_int2(v.x * rc.neg_one, v.y * rc.neg_one);
                 win[0] = make_int4(v.x, v.y, v.x + v.y, 0);
             }
         }
