@@ -67,10 +67,22 @@ GFP_HD u64 w_pow(u64 a, u64 e, const WordConsts &c)
     return acc;
 }
 
+// x * w mod q for a constant w (standard form) with its Shoup factor
+// ws = floor(w 2^64 / q): one high and two low 64-bit products instead of
+// REDC's three wide ones.  With w = the standard value of a Montgomery
+// constant w_m (w = w_m R^-1), x * w = mont_mul(x, w_m): the same residue,
+// so Montgomery-form data keeps its form.
+GFP_D u64 w_mul_shoup(u64 x, ulonglong2 w, const WordConsts &c)
+{
+    const u64 hi = __umul64hi(x, w.y);
+    const u64 r = x * w.x - hi * c.q;  // in [0, 2q)
+    return r >= c.q ? r - c.q : r;
+}
+
 struct WordPassArgs {
     const u64 *in;
     u64 *out;
-    const u64 *tw;     // w^i, i < N (Montgomery)
+    const ulonglong2 *tw;  // {w^i (standard form), Shoup factor}, i < N
     const u64 *w_in;   // pass 0: x_i <- x_i * w_in[i] (nullptr: none)
     const u64 *pre;    // pass 0: x_i <- x_i * pre[b][i] (pointwise operand)
     const u64 *w_out;  // last pass: X_u <- X_u * w_out[u]
@@ -82,7 +94,7 @@ struct WordPassArgs {
 
 // w^(e) for the R-point DFT factor, e in units of N / R
 template <int R>
-GFP_D u64 w_root(const WordPassArgs &A, int e)
+GFP_D ulonglong2 w_root(const WordPassArgs &A, int e)
 {
     return __ldg(A.tw + ((int64_t)e << (A.lN - (R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1))));
 }
@@ -138,7 +150,7 @@ __global__ void __launch_bounds__(256) k_word_pass(WordPassArgs A)
     if (js) {  // w^(t js M / Ns)
 #pragma unroll
         for (int t = 1; t < R; t++)
-            x[t] = w_mul(x[t], __ldg(A.tw + (((int64_t)t * js) << (A.lN - LR - A.lNs))), c);
+            x[t] = w_mul_shoup(x[t], __ldg(A.tw + (((int64_t)t * js) << (A.lN - LR - A.lNs))), c);
     }
     // R-point DFT at root w^(N/R): decimation in time, bit-reversed input
     // order resolved at compile time
@@ -154,7 +166,7 @@ __global__ void __launch_bounds__(256) k_word_pass(WordPassArgs A)
             u64 u = y[lo], v = y[lo + half];
             const int e = m << (LR - s);  // w_R^(m R / 2^s)
             if (e)
-                v = w_mul(v, w_root<R>(A, e), c);
+                v = w_mul_shoup(v, w_root<R>(A, e), c);
             y[lo] = w_add(u, v, c);
             y[lo + half] = w_sub(u, v, c);
         }
@@ -205,6 +217,27 @@ __global__ void k_word_powers(u64 *table, int64_t n, u64 base, u64 post, WordCon
         table[i] = w_mul(w_pow(base, (u64)i, c), post, c);
 }
 
+// table[i] = {w, floor(w 2^64 / q)} with w = base^i in standard form
+// (base Montgomery); the quotient by restoring long division (plan time)
+__global__ void k_word_shoup_powers(ulonglong2 *table, int64_t n, u64 base, WordConsts c)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const u64 w = w_mul(w_pow(base, (u64)i, c), 1, c);  // standard form
+        u64 rem = w, quo = 0;  // (w 2^64) / q, one quotient bit per step
+        for (int b = 0; b < 64; b++) {
+            const bool top = rem >> 63;
+            rem <<= 1;
+            quo <<= 1;
+            if (top || rem >= c.q) {
+                rem -= c.q;
+                quo |= 1;
+            }
+        }
+        table[i] = make_ulonglong2(w, quo);
+    }
+}
+
 __global__ void k_word_mul(const u64 *a, const u64 *b, u64 *z, int64_t n, WordConsts c)
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -224,7 +257,7 @@ struct gfp_word_plan {
     WordConsts c;
     int64_t n;
     int lN;
-    u64 *tw_fwd, *tw_inv;  // w^i, w^-i (i < n)
+    ulonglong2 *tw_fwd, *tw_inv;  // {w^i, Shoup}, {w^-i, Shoup} (i < n), standard form
     u64 ninv;              // n^-1 in Montgomery form
     u64 *w_in, *w_out;     // convolution weights (standard-form in/out), or null
     u64 *scratch;
@@ -383,16 +416,16 @@ int gfp_word_plan_create(gfp_word_plan **plan, uint64_t q, int64_t n, uint64_t o
     const u64 omega_inv = w_pow(omega, (u64)n - 1, c);
     const u64 n_m = w_mul((u64)(n % (int64_t)q), c.r2, c);
     p->ninv = w_pow(n_m, q - 2, c);  // (n^-1) R
-    if (cudaMalloc(&p->tw_fwd, sizeof(u64) * n) != cudaSuccess ||
-        cudaMalloc(&p->tw_inv, sizeof(u64) * n) != cudaSuccess ||
+    if (cudaMalloc(&p->tw_fwd, sizeof(ulonglong2) * n) != cudaSuccess ||
+        cudaMalloc(&p->tw_inv, sizeof(ulonglong2) * n) != cudaSuccess ||
         cudaMalloc(&p->w_in, sizeof(u64) * n) != cudaSuccess ||
         cudaMalloc(&p->w_out, sizeof(u64) * n) != cudaSuccess) {
         gfp_word_plan_destroy(p);
         return GFP_ENOMEM;
     }
     const dim3 g = grid_for(n, 256);
-    k_word_powers<<<g, 256, 0, st>>>(p->tw_fwd, n, omega, c.one, c);
-    k_word_powers<<<g, 256, 0, st>>>(p->tw_inv, n, omega_inv, c.one, c);
+    k_word_shoup_powers<<<g, 256, 0, st>>>(p->tw_fwd, n, omega, c);
+    k_word_shoup_powers<<<g, 256, 0, st>>>(p->tw_inv, n, omega_inv, c);
     // convolution weights (gfp_mult.py:280-323): standard-form inputs enter
     // Montgomery form with the weight, outputs leave it with the 1/n scale
     //   cyclic:     in_i = R^2,             out_i = n^-1          (standard)
