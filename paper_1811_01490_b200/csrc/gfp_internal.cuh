@@ -27,6 +27,7 @@ struct PassArgs {
     u64 *out;
     const u64 *table;  // element-major [M][k] balanced, omega^b (or omega^b / N)
     const u64 *table_lh;  // the same entries as limb pairs l | h << 32 (k_pass44)
+    const u64 *table_lh_plain;  // omega^b limb pairs even when scale (k_pass256's outer twiddle)
     const u64 *pre;    // optional pointwise operand, digit-major like `in`
     const u64 *in2;    // optional second set of `batch` vectors (grid.y >= batch)
     u64 *out2;
@@ -97,6 +98,8 @@ struct gfp_fft_plan {
 // one radix-K Stockham pass (gfp_pass.cuh), instantiated per k in gfp_pass_k*.cu
 // true when the pass kernels of this plan take element-major I/O (PassIO)
 bool em_io_supported(const gfp_fft_plan *p);
+// true when pairs of passes run as one k_pass256 launch (k = 8, mode 3, N >= 1024)
+bool pass256_ok(const gfp_fft_plan *p);
 
 // em: element-major first-pass input / last-pass output (nullptr: none);
 // returns GFP_EUNSUPPORTED when em is requested but the kernel for this k
@@ -105,6 +108,13 @@ template <int KD>
 int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2, u64 *out2,
                 const u64 *pre, int64_t batch, int64_t Ns, int inverse, int scale, int canon,
                 int in_canon, const PassIO *em, cudaStream_t st);
+
+// two consecutive passes (Ns, K Ns) in one launch (k_pass256; k = 8 only):
+// GFP_EUNSUPPORTED when the pair kernel does not apply
+template <int KD>
+int launch_pass_pair(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2, u64 *out2,
+                     const u64 *pre, int64_t batch, int64_t Ns, int inverse, int scale,
+                     int canon, int in_canon, cudaStream_t st);
 
 #define DISPATCH_K(k, CALL)                                                                     \
     switch (k) {                                                                                \

@@ -10,7 +10,7 @@
 #pragma once
 #include "gfp_internal.cuh"
 #include "gfp_fast.cuh"
-#include "gfp_pass44.cuh"
+#include "gfp_pass256.cuh"
 
 // k values whose pass multiply keeps the twiddle limbs in shared memory
 // (fast_mul_window_store) instead of registers
@@ -293,35 +293,20 @@ static size_t pass_smem(int G)
            (PASS_WINDOW(KD) ? (size_t)KD * G * KD * sizeof(int2) : 0);
 }
 
-template <int KD>
-int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
-                       u64 *out2, const u64 *pre, int64_t batch, int64_t Ns, int inverse,
-                       int scale, int canon, int in_canon, const PassIO *em, cudaStream_t st)
+// the pass-kernel arguments shared by k_pass, k_pass44 and k_pass256
+static inline int make_pass_args(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
+                                 u64 *out2, const u64 *pre, int64_t batch, int64_t Ns,
+                                 int inverse, int scale, int canon, int in_canon,
+                                 const PassIO *em, int G, PassArgs &A)
 {
-    int G;
-    int threads = pass_threads(KD, p->M, &G);
-    size_t smem = pass_smem<KD>(G);
-    static bool attr_set = false;
-    if (!attr_set) {
-        for (int m = 0; m < 3; m++) {
-            const void *fn = m == 0 ? (const void *)k_pass<KD, 0>
-                             : m == 1 ? (const void *)k_pass<KD, 1> : (const void *)k_pass<KD, 2>;
-            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)pass_smem<KD>(256 / KD));
-        }
-        if constexpr (P2Radix<KD>::a != 0)
-            cudaFuncSetAttribute((const void *)k_pass<KD, 3>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)pass_smem<KD>(256 / KD));
-        attr_set = true;
-    }
-    PassArgs A;
+    A.gpc = 32;
     A.in = in;
     A.out = out;
     A.table = scale ? p->table_ninv : p->table;
     A.table_lh = scale ? p->table_ninv_lh : p->table_lh;
+    A.table_lh_plain = p->table_lh;
     A.pre = pre;
-    A.batch_stride = (int64_t)KD * p->N;
+    A.batch_stride = (int64_t)p->k * p->N;
     A.lN = ilog2_exact(p->N);
     A.lM = ilog2_exact(p->M);
     A.lNs = ilog2_exact(Ns);
@@ -364,6 +349,36 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
             A.n_out = em->n_out;
         }
     }
+    return GFP_OK;
+}
+
+template <int KD>
+int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
+                       u64 *out2, const u64 *pre, int64_t batch, int64_t Ns, int inverse,
+                       int scale, int canon, int in_canon, const PassIO *em, cudaStream_t st)
+{
+    int G;
+    int threads = pass_threads(KD, p->M, &G);
+    size_t smem = pass_smem<KD>(G);
+    static bool attr_set = false;
+    if (!attr_set) {
+        for (int m = 0; m < 3; m++) {
+            const void *fn = m == 0 ? (const void *)k_pass<KD, 0>
+                             : m == 1 ? (const void *)k_pass<KD, 1> : (const void *)k_pass<KD, 2>;
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)pass_smem<KD>(256 / KD));
+        }
+        if constexpr (P2Radix<KD>::a != 0)
+            cudaFuncSetAttribute((const void *)k_pass<KD, 3>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)pass_smem<KD>(256 / KD));
+        attr_set = true;
+    }
+    PassArgs A;
+    int err = make_pass_args(p, in, out, in2, out2, pre, batch, Ns, inverse, scale, canon, in_canon,
+                             em, G, A);
+    if (err)
+        return err;
     if (launch_pass44<KD>(A, p->M, in2 ? 2 * batch : batch, st))
         return cuda_status();
     if (A.in_em || A.out_em || A.ft_lh)
@@ -383,4 +398,27 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
         launch_pdl(k_pass<KD, 0>, grid, threads, st, A, smem);
     }
     return cuda_status();
+}
+
+// Two consecutive passes (Ns, 16 Ns) in one k_pass256 launch (k = 8, mode 3,
+// N >= 1024, no element-major / four-step I/O, not both the pointwise
+// operand and N^-1): GFP_EUNSUPPORTED otherwise (the caller runs two passes)
+template <int KD>
+int launch_pass_pair(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2, u64 *out2,
+                     const u64 *pre, int64_t batch, int64_t Ns, int inverse, int scale,
+                     int canon, int in_canon, cudaStream_t st)
+{
+    if constexpr (KD != 8) {
+        return GFP_EUNSUPPORTED;
+    } else {
+        if (!pass256_enabled(KD, p->rc, p->N) || (pre && scale))
+            return GFP_EUNSUPPORTED;
+        PassArgs A;
+        int err = make_pass_args(p, in, out, in2, out2, pre, batch, Ns, inverse, scale, canon,
+                                 in_canon, nullptr, 1, A);
+        if (err)
+            return err;
+        launch_pass256(A, p->N, in2 ? 2 * batch : batch, st);
+        return cuda_status();
+    }
 }

@@ -178,12 +178,28 @@ static int run_transform2(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, c
                           u64 *out_b, u64 *work_b, const u64 *pre, int64_t batch, int inverse,
                           int in_canon, int out_canon, cudaStream_t st, const PassIO *em = nullptr)
 {
-    // ping-pong so that the last pass lands in `out`; inputs are never written
-    int e = p->e;
+    // launch schedule: pairs of passes in one k_pass256 launch where it
+    // applies (not the element-major first / last pass of the host paths,
+    // not a four-step first pass), single passes otherwise
+    const int e = p->e;
+    int span[64], nl = 0;
+    {
+        int pass = 0;
+        while (pass < e) {
+            const bool em_first = em && pass == 0 && (em->in || em->ft);
+            const bool em_last = em && pass + 1 == e - 1 && em->out && out_canon;
+            const bool pair = pass + 1 < e && !em_first && !em_last && p->k == 8 &&
+                              pass256_ok(p) && !(pass == 0 && pre && inverse && pass + 1 == e - 1);
+            span[nl++] = pair ? 2 : 1;
+            pass += pair ? 2 : 1;
+        }
+    }
+    // ping-pong so that the last launch lands in `out`; inputs are never written
     const u64 *src = in, *src_b = in_b;
     int64_t Ns = 1;
-    for (int pass = 0; pass < e; pass++) {
-        int remaining = e - pass;  // passes left including this one
+    int pass = 0;
+    for (int l = 0; l < nl; l++) {
+        const int remaining = nl - l;  // launches left including this one
         u64 *dst = (remaining % 2 == 1) ? out : work;
         if (dst == src)
             dst = (dst == out) ? work : out;
@@ -193,19 +209,28 @@ static int run_transform2(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, c
             if (dst_b == src_b)
                 dst_b = (dst_b == out_b) ? work_b : out_b;
         }
-        int last = pass == e - 1;
-        int scale = inverse && last;
+        const int last = pass + span[l] == e;
+        const int scale = inverse && last;
         const u64 *pre_p = pass == 0 ? pre : nullptr;
-        int rcode;
-        DISPATCH_FAST_K(p->k, (rcode = launch_pass<KD>(p, src, dst, src_b, dst_b, pre_p, batch,
-                                                       Ns, inverse, scale, last && out_canon,
-                                                       pass == 0 && in_canon, em, st)));
+        int rcode = GFP_EUNSUPPORTED;
+        if (span[l] == 2) {
+            DISPATCH_FAST_K(p->k, (rcode = launch_pass_pair<KD>(p, src, dst, src_b, dst_b, pre_p,
+                                                                batch, Ns, inverse, scale,
+                                                                last && out_canon,
+                                                                pass == 0 && in_canon, st)));
+        } else {
+            DISPATCH_FAST_K(p->k, (rcode = launch_pass<KD>(p, src, dst, src_b, dst_b, pre_p, batch,
+                                                           Ns, inverse, scale, last && out_canon,
+                                                           pass == 0 && in_canon, em, st)));
+        }
         if (rcode)
             return rcode;
         p->last_launches++;
         src = dst;
         src_b = dst_b;
-        Ns *= p->K;
+        for (int i = 0; i < span[l]; i++)
+            Ns *= p->K;
+        pass += span[l];
     }
     if (em && em->out && out_canon)
         return cuda_status();  // the last pass wrote the element-major output
