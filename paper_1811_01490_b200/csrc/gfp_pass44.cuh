@@ -35,6 +35,12 @@
 #ifndef P44_MINB
 #define P44_MINB 5  // CTAs per SM the NW = 4 variant is register-bounded for (96 regs)
 #endif
+#ifndef P44_AUNROLL
+#define P44_AUNROLL 1  // phase-A elements interleaved per thread (experiment hook)
+#endif
+#define P44_STR_(x) #x
+#define P44_UNROLL_(n) _Pragma(P44_STR_(unroll n))
+#define P44_UNROLL(n) P44_UNROLL_(n)
 #ifndef P44_PF_MINNW
 #define P44_PF_MINNW 8  // smallest NW that stages the next element with cp.async (NW = 4
                         // keeps 40 KB smem for 5 CTAs / SM: measured 1.5% faster on C4)
@@ -232,7 +238,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
     if (pf)
         prefetch(0);
     i64 e[4][KD];
-#pragma unroll 1
+    P44_UNROLL(P44_AUNROLL)
     for (int i = 0; i < 16 / NW; i++) {
         const int t = w + NW * i;
         i64 f[KD], x[KD];
