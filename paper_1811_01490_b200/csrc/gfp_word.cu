@@ -182,6 +182,25 @@ __global__ void __launch_bounds__(256) k_word_pass(WordPassArgs A)
         for (int u = 0; u < R; u++)
             y[u] = w_mul(y[u], A.scale, c);
     }
+    if (R == 16 && A.lNs == 0 && (j | 31) < M) {
+        // first pass: thread j writes positions 16 j .. 16 j + 15 -- stage the
+        // warp's 512 outputs in shared memory and store them contiguously
+        // (a lane-per-group store touches 32 lines with 8 bytes each)
+        __shared__ u64 stage[8][32 * 17];
+        const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+        u64 *st = stage[wq];
+#pragma unroll
+        for (int u = 0; u < R; u++)
+            st[lane * 17 + u] = y[u];
+        __syncwarp();
+        u64 *ob = out + ((j - lane) << 4);
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            const int q = lane + 32 * i;  // position 16 (j - lane) + q
+            __stcs(ob + q, st[(q >> 4) * 17 + (q & 15)]);
+        }
+        return;
+    }
 #pragma unroll
     for (int u = 0; u < R; u++)
         __stcs(out + obase + ((int64_t)u << A.lNs), y[u]);
