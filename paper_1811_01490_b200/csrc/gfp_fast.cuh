@@ -189,6 +189,12 @@ struct ColReduce {
     }
 };
 
+// v or -v by a sign mask m in {0, -1}: (v ^ m) - m, two ALU instructions
+// (LOP3 + IADD3).  A multiply by +-1 would sit on the FMA-heavy pipe that the
+// IMAD.WIDE products saturate; a literal negation gets folded into the
+// products by ptxas (see RadixConsts::neg_one).
+GFP_D int cond_neg(int v, int m) { return (v ^ m) - m; }
+
 // x * y mod p for balanced lazy digits (|digit| <= r/2 + delta), output
 // balanced lazy digits.  Limbs are balanced too, x = xh 2^S + xl with
 // xl in [-2^(S-1), 2^(S-1)), and the middle sub-column comes from one
@@ -294,9 +300,9 @@ GFP_D void fast_mul_lazy(const i64 (&x)[KD], const i64 (&y)[KD], i64 (&f)[KD],
     for (int i = 0; i < KD; i++) {
         int l0, h0;
         split_limbs<S>(x[i], l0, h0);
-        const int sg = 1 - (int)((negx >> i) & 1u) * 2;
-        xh[i] = h0 * sg;
-        xl[i] = l0 * sg;
+        const int sm = -(int)((negx >> i) & 1u);  // 0 or -1
+        xh[i] = cond_neg(h0, sm);
+        xl[i] = cond_neg(l0, sm);
         xs[i] = xl[i] + xh[i];
         split_limbs<S>(y[i], yl[i], yh[i]);
         ys[i] = yl[i] + yh[i];
@@ -316,9 +322,9 @@ GFP_D void fast_mul_lazy_ylimbs(const i64 (&x)[KD], const u64 (&ylh)[KD], i64 (&
     for (int i = 0; i < KD; i++) {
         int l0, h0;
         split_limbs<S>(x[i], l0, h0);
-        const int sg = 1 - (int)((negx >> i) & 1u) * 2;
-        xh[i] = h0 * sg;
-        xl[i] = l0 * sg;
+        const int sm = -(int)((negx >> i) & 1u);  // 0 or -1
+        xh[i] = cond_neg(h0, sm);
+        xl[i] = cond_neg(l0, sm);
         xs[i] = xl[i] + xh[i];
         yl[i] = (int)(unsigned)ylh[i];
         yh[i] = (int)(unsigned)(ylh[i] >> 32);
@@ -343,9 +349,9 @@ GFP_D void fast_mul_window_store(const i64 (&x)[KD], unsigned negx, const int2 *
     for (int i = 0; i < KD; i++) {
         int l0, h0;
         split_limbs<S>(x[i], l0, h0);
-        const int sg = 1 - (int)((negx >> i) & 1u) * 2;
-        xh[i] = h0 * sg;
-        xl[i] = l0 * sg;
+        const int sm = -(int)((negx >> i) & 1u);  // 0 or -1
+        xh[i] = cond_neg(h0, sm);
+        xl[i] = cond_neg(l0, sm);
         xs[i] = xl[i] + xh[i];
     }
     ColReduce<S, SPARSE, KD> cr;
@@ -379,7 +385,7 @@ GFP_D void fast_mul_window_store(const i64 (&x)[KD], unsigned negx, const int2 *
                 const int j = m0 - i - 1;
                 int2 v = ywin[((j + KD) & (KD - 1)) * stride];
                 if (j < 0)  // r^k = -1 (rc.neg_one: see RadixConsts)
-                    v = make_int2(v.x * rc.neg_one, v.y * rc.neg_one);
+                    v = make_int2(cond_neg(v.x, rc.neg_one), cond_neg(v.y, rc.neg_one));
                 win[0] = make_int4(v.x, v.y, v.x + v.y, 0);
             }
         }

@@ -281,6 +281,8 @@ struct gfp_word_plan {
     u64 *w_in, *w_out;     // convolution weights (standard-form in/out), or null
     u64 *scratch;
     int64_t scratch_words;
+    int *d_bad;  // input range flag (device) and its pinned host copy
+    int *h_bad;
 };
 
 static WordConsts word_consts(u64 q)
@@ -476,6 +478,9 @@ int gfp_word_plan_destroy(gfp_word_plan *p)
     cudaFree(p->w_in);
     cudaFree(p->w_out);
     cudaFree(p->scratch);
+    cudaFree(p->d_bad);
+    if (p->h_bad)
+        cudaFreeHost(p->h_bad);
     free(p);
     return GFP_OK;
 }
@@ -502,18 +507,15 @@ int gfp_word_convolve(gfp_word_plan *p, const uint64_t *x, const uint64_t *y, ui
     int err = ensure_scratch(p, 3 * words);
     if (err)
         return err;
-    int *bad;
-    if (cudaMallocAsync((void **)&bad, sizeof(int), st) != cudaSuccess)
-        return GFP_ENOMEM;
-    cudaMemsetAsync(bad, 0, sizeof(int), st);
-    k_word_check<<<grid_for(words, 256), 256, 0, st>>>(x, words, p->c.q, bad);
-    k_word_check<<<grid_for(words, 256), 256, 0, st>>>(y, words, p->c.q, bad);
-    int hbad = 0;
-    cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
-    cudaFreeAsync(bad, st);
-    cudaStreamSynchronize(st);
-    if (hbad)
-        return GFP_EINVAL;  // "inputs must be reduced mod q" (gfp_mult.py:361-366)
+    if (!p->d_bad) {
+        if (cudaMalloc((void **)&p->d_bad, sizeof(int)) != cudaSuccess ||
+            cudaMallocHost((void **)&p->h_bad, sizeof(int)) != cudaSuccess)
+            return GFP_ENOMEM;
+    }
+    // range check queued with the work; one synchronisation at the end
+    cudaMemsetAsync(p->d_bad, 0, sizeof(int), st);
+    k_word_check<<<grid_for(words, 256), 256, 0, st>>>(x, words, p->c.q, p->d_bad);
+    k_word_check<<<grid_for(words, 256), 256, 0, st>>>(y, words, p->c.q, p->d_bad);
     u64 *a = p->scratch, *b = p->scratch + words, *work = p->scratch + 2 * words;
     // forward of both weighted operands, then the inverse with the pointwise
     // product fused into its first pass and the out weights into its last
@@ -522,7 +524,13 @@ int gfp_word_convolve(gfp_word_plan *p, const uint64_t *x, const uint64_t *y, ui
         err = word_run(p, y, b, batch, 0, p->w_in, nullptr, nullptr, 0, work, st);
     if (!err)
         err = word_run(p, a, out, batch, 1, nullptr, b, p->w_out, 0, work, st);
-    return err;
+    if (err)
+        return err;
+    cudaMemcpyAsync(p->h_bad, p->d_bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess)
+        return cuda_status();
+    // "inputs must be reduced mod q" (gfp_mult.py:361-366); out is unspecified then
+    return *p->h_bad ? GFP_EINVAL : GFP_OK;
 }
 
 }  // extern "C"

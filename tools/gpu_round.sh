@@ -14,3 +14,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 python tools/ncu_summary.py launches gpurun_out/launches.csv > gpurun_out/launches_summary.txt 2>&1
 bash tools/gpu_prof.sh c2 8 8 c2 k_pass 786432
 bash tools/gpu_prof.sh c4 7 1 c4 k_pass 16777216
+python tools/ncu_pipes.py /tmp/prof_c4_raw.csv > gpurun_out/pipes_c4.txt 2>&1
