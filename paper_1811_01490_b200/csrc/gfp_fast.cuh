@@ -195,6 +195,19 @@ struct ColReduce {
 // products by ptxas (see RadixConsts::neg_one).
 GFP_D int cond_neg(int v, int m) { return (v ^ m) - m; }
 
+#ifndef GFP_NEG_X_ALU
+#define GFP_NEG_X_ALU 0  // x-limb signs by cond_neg (else a multiply by +-1; measured equal for k = 8)
+#endif
+#ifndef GFP_NEG_WIN_ALU
+#define GFP_NEG_WIN_ALU 0  // window digit signs by cond_neg (else * rc.neg_one; the multiply
+                         // measured 2% faster for C3 although it sits on the FMA-heavy pipe)
+#endif
+GFP_D int sign_x(int v, unsigned bit)
+{
+    return GFP_NEG_X_ALU ? cond_neg(v, -(int)bit) : v * (1 - 2 * (int)bit);
+}
+GFP_D int sign_win(int v, int neg_one) { return GFP_NEG_WIN_ALU ? cond_neg(v, neg_one) : v * neg_one; }
+
 // x * y mod p for balanced lazy digits (|digit| <= r/2 + delta), output
 // balanced lazy digits.  Limbs are balanced too, x = xh 2^S + xl with
 // xl in [-2^(S-1), 2^(S-1)), and the middle sub-column comes from one
@@ -300,9 +313,9 @@ GFP_D void fast_mul_lazy(const i64 (&x)[KD], const i64 (&y)[KD], i64 (&f)[KD],
     for (int i = 0; i < KD; i++) {
         int l0, h0;
         split_limbs<S>(x[i], l0, h0);
-        const int sm = -(int)((negx >> i) & 1u);  // 0 or -1
-        xh[i] = cond_neg(h0, sm);
-        xl[i] = cond_neg(l0, sm);
+        const unsigned sb = (negx >> i) & 1u;
+        xh[i] = sign_x(h0, sb);
+        xl[i] = sign_x(l0, sb);
         xs[i] = xl[i] + xh[i];
         split_limbs<S>(y[i], yl[i], yh[i]);
         ys[i] = yl[i] + yh[i];
@@ -322,9 +335,9 @@ GFP_D void fast_mul_lazy_ylimbs(const i64 (&x)[KD], const u64 (&ylh)[KD], i64 (&
     for (int i = 0; i < KD; i++) {
         int l0, h0;
         split_limbs<S>(x[i], l0, h0);
-        const int sm = -(int)((negx >> i) & 1u);  // 0 or -1
-        xh[i] = cond_neg(h0, sm);
-        xl[i] = cond_neg(l0, sm);
+        const unsigned sb = (negx >> i) & 1u;
+        xh[i] = sign_x(h0, sb);
+        xl[i] = sign_x(l0, sb);
         xs[i] = xl[i] + xh[i];
         yl[i] = (int)(unsigned)ylh[i];
         yh[i] = (int)(unsigned)(ylh[i] >> 32);
@@ -349,9 +362,9 @@ GFP_D void fast_mul_window_store(const i64 (&x)[KD], unsigned negx, const int2 *
     for (int i = 0; i < KD; i++) {
         int l0, h0;
         split_limbs<S>(x[i], l0, h0);
-        const int sm = -(int)((negx >> i) & 1u);  // 0 or -1
-        xh[i] = cond_neg(h0, sm);
-        xl[i] = cond_neg(l0, sm);
+        const unsigned sb = (negx >> i) & 1u;
+        xh[i] = sign_x(h0, sb);
+        xl[i] = sign_x(l0, sb);
         xs[i] = xl[i] + xh[i];
     }
     ColReduce<S, SPARSE, KD> cr;
@@ -385,7 +398,7 @@ GFP_D void fast_mul_window_store(const i64 (&x)[KD], unsigned negx, const int2 *
                 const int j = m0 - i - 1;
                 int2 v = ywin[((j + KD) & (KD - 1)) * stride];
                 if (j < 0)  // r^k = -1 (rc.neg_one: see RadixConsts)
-                    v = make_int2(cond_neg(v.x, rc.neg_one), cond_neg(v.y, rc.neg_one));
+                    v = make_int2(sign_win(v.x, rc.neg_one), sign_win(v.y, rc.neg_one));
                 win[0] = make_int4(v.x, v.y, v.x + v.y, 0);
             }
         }
