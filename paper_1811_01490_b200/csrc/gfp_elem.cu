@@ -205,6 +205,8 @@ RadixConsts make_consts(int k, u64 r)
             norm_bounds(3 * (u128)r, r, fp, &q2, &ex2);
             norm_bounds(X + cmax, r, fp, &q0, &ex0);
             ok = ok && ex0 <= fp.delta && ex2 + q0 <= fp.delta;
+            // the k = 32 mode-3 pass runs its 64-point DFT without a mid normalisation
+            ok = ok && (k != 32 || fp.S >= 6);
             c.p3_ok = ok ? 1 : 0;
         }
     } else {

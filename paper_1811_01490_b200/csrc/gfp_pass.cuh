@@ -18,11 +18,17 @@
 #define PASS_WINDOW_MINK 16
 #endif
 #ifndef PASS_WINDOW_MAXK
-#define PASS_WINDOW_MAXK 16
+#define PASS_WINDOW_MAXK 32  // k = 32 too (200 registers, no spills: C5 FFT 0.61 -> 0.52 ms)
 #endif
 #define PASS_WINDOW(KD) ((KD) >= PASS_WINDOW_MINK && (KD) <= PASS_WINDOW_MAXK)
 #ifndef GFP_WINDOW_CC
 #define GFP_WINDOW_CC true
+#endif
+#ifndef P32_SPLIT
+#define P32_SPLIT 1  // k = 32: the 64-point DFT as 8 x 8 (eight live values per lane)
+#endif
+#ifndef PASS32_MINB
+#define PASS32_MINB 2
 #endif
 #ifndef PASS16_MINB
 #define PASS16_MINB 3  // CTAs per SM the k = 16 pass is register-bounded for
@@ -50,6 +56,44 @@ GFP_D void normalize_lane(i64 &v, int d, const RadixConsts &rc)
     v = rem + (d == 0 ? -qin : qin);
 }
 
+// x * r^e for any 0 <= e < 2k on a digit held one-digit-per-lane
+// (r^k = -1: e >= k negates)
+template <int KD>
+GFP_D i64 rot_lane_any(i64 val, int e, int d, bool inverse)
+{
+    const bool flip = (e & KD) != 0;
+    const int t = e & (KD - 1);
+    i64 v = t ? rot_lane<KD>(val, t, d, inverse) : val;
+    return flip ? -v : v;
+}
+
+// 8-point DFT at root r^(8 s) -- s = rstep / 8 -- of digit lanes, natural
+// order in and out (decimation in frequency, compile-time bit reversal)
+template <int KD, int RSTEP>
+GFP_D void dft8_lane(i64 (&v)[8], int d, bool inverse)
+{
+#pragma unroll
+    for (int len = 4; len >= 1; len >>= 1) {
+#pragma unroll
+        for (int st = 0; st < 8; st += 2 * len) {
+#pragma unroll
+            for (int i = 0; i < len; i++) {
+                const i64 a0 = v[st + i], b0 = v[st + i + len];
+                v[st + i] = a0 + b0;
+                const int e = RSTEP * i * (8 / (2 * len));  // < 2k
+                v[st + i + len] = e ? rot_lane_any<KD>(a0 - b0, e, d, inverse) : a0 - b0;
+            }
+        }
+    }
+    i64 w[8];
+#pragma unroll
+    for (int t = 0; t < 8; t++)
+        w[t] = v[t];
+#pragma unroll
+    for (int t = 0; t < 8; t++)
+        v[((t & 1) << 2) | (t & 2) | ((t >> 2) & 1)] = w[t];
+}
+
 template <int K>
 __host__ __device__ constexpr int bitrev_c(int x)
 {
@@ -67,7 +111,8 @@ __host__ __device__ constexpr int bitrev_c(int x)
 // (j / Ns) Ns K + (j mod Ns) + u Ns.  After log_K N passes the output is the
 // natural-order DFT (the reference's dft_general result, fft.py:298-360).
 template <int KD, int SPARSE>
-__global__ void __launch_bounds__(KD >= 16 ? 128 : 256, KD == 16 ? PASS16_MINB : 1)
+__global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
+                                  KD == 16 ? PASS16_MINB : KD == 32 ? PASS32_MINB : 1)
     k_pass(PassArgs A)
 {
     constexpr int K = 2 * KD;
@@ -134,11 +179,32 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256, KD == 16 ? PASS16_MINB :
             if (A.in_canon)  // pass 0 only, where a = 0
                 to_balanced<KD>(x, rc.r);
             if (pre) {  // pass 0 only (a = b = 0)
-                i64 y[KD];
+                if constexpr (KD == 32 && PASS_WINDOW(KD)) {
+                    // through the window (registers: x only), product parked in
+                    // the element's row and read back
+                    constexpr int S = FastSplit<KD>::S;
+                    unsigned long long *yw =
+                        reinterpret_cast<unsigned long long *>(sm + ((size_t)K << lG) * ROW) + tid;
+                    const int nt = (int)blockDim.x;
 #pragma unroll
-                for (int d = 0; d < KD; d++)
-                    y[d] = (i64)__ldg(pre + ((int64_t)d << lN) + pos);
-                fast_mul_lazy<KD, SPARSE>(x, y, x, rc);
+                    for (int d = 0; d < KD; d++) {
+                        int l, h;
+                        split_limbs<S>((i64)__ldg(pre + ((int64_t)d << lN) + pos), l, h);
+                        yw[d * nt] = (u64)(unsigned)l | ((u64)(unsigned)h << 32);
+                    }
+                    i64 *prow = sm + (((int64_t)t << lG) + g) * ROW;
+                    fast_mul_window_store<KD, SPARSE, GFP_WINDOW_CC>(
+                        x, 0u, reinterpret_cast<const int2 *>(yw), nt, prow, rc);
+#pragma unroll
+                    for (int d = 0; d < KD; d++)
+                        x[d] = prow[d];
+                } else {
+                    i64 y[KD];
+#pragma unroll
+                    for (int d = 0; d < KD; d++)
+                        y[d] = (i64)__ldg(pre + ((int64_t)d << lN) + pos);
+                    fast_mul_lazy<KD, SPARSE>(x, y, x, rc);
+                }
             }
         } else {
 #pragma unroll
@@ -190,7 +256,44 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256, KD == 16 ? PASS16_MINB :
     __syncthreads();
 
     // ---- phase B: K-point DFT at root r (or 1/r), one digit per lane
-    {
+    if constexpr (KD == 32 && P32_SPLIT && SPARSE == 3) {  // mode 3: S = 6 (p3_ok)
+        // K = 64 = 8 x 8 (t = t1 + 8 t2, u = u0 + 8 u1): 8-point DFTs over t2
+        // in place, the factor rho^(t1 u0) (a lane rotation), 8-point DFTs
+        // over t1 with X[u0 + 8 u1] left in slot u1 + 8 u0 (the slots this
+        // step read); eight values per lane live at a time instead of 64.
+        // One warp owns a group's slots: warp barriers only.
+        const int d = tid & (KD - 1);
+        const int g = tid / KD;
+        const bool inv = A.rot_inv != 0;
+        i64 *gs = sm + (int64_t)g * ROW + d;  // slot t at gs[(t << lG) * ROW]
+#pragma unroll 1
+        for (int t1 = 0; t1 < 8; t1++) {
+            i64 v[8];
+#pragma unroll
+            for (int t2 = 0; t2 < 8; t2++)
+                v[t2] = gs[((int64_t)(t1 + 8 * t2) << lG) * ROW];
+            dft8_lane<KD, 8>(v, d, inv);
+#pragma unroll
+            for (int u0 = 0; u0 < 8; u0++)
+                gs[((int64_t)(t1 + 8 * u0) << lG) * ROW] = v[u0];
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (int u0 = 0; u0 < 8; u0++) {
+            i64 v[8];
+#pragma unroll
+            for (int t1 = 0; t1 < 8; t1++) {
+                const i64 y = gs[((int64_t)(t1 + 8 * u0) << lG) * ROW];
+                v[t1] = t1 ? rot_lane_any<KD>(y, (t1 * u0) & (2 * KD - 1), d, inv) : y;
+            }
+            dft8_lane<KD, 8>(v, d, inv);
+#pragma unroll
+            for (int u1 = 0; u1 < 8; u1++) {
+                normalize_lane<KD, SPARSE>(v[u1], d, rc);
+                gs[((int64_t)(u1 + 8 * u0) << lG) * ROW] = v[u1];
+            }
+        }
+    } else {
         const int d = tid & (KD - 1);
         const int g = tid / KD;
         const bool inv = A.rot_inv != 0;
@@ -231,6 +334,7 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256, KD == 16 ? PASS16_MINB :
     __syncthreads();
 
     // ---- phase C: store in Stockham order (canonicalise on the last pass)
+    // (the k = 32 split DFT leaves X[u0 + 8 u1] in slot u1 + 8 u0)
 #pragma unroll 1
     for (int h = 0; h < 2; h++) {
         const int g = tid & (G - 1);
@@ -239,7 +343,8 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256, KD == 16 ? PASS16_MINB :
         if (j >= M)
             continue;
         const int64_t pos = ((j >> lNs) << (lNs + LK)) + (j & nsmask) + ((int64_t)u << lNs);
-        const i64 *row = sm + (((int64_t)u << lG) + g) * ROW;
+        const int us = (KD == 32 && P32_SPLIT && SPARSE == 3) ? ((u >> 3) | ((u & 7) << 3)) : u;
+        const i64 *row = sm + (((int64_t)us << lG) + g) * ROW;
         if (A.canon) {
             i64 f[KD];
             u64 c[KD];
