@@ -540,10 +540,37 @@ def multi_gpu_configs(args, ws, rank, dev, flush, stream):
                              "n_gpus": ws, "ms_fwd": ms, "elements_per_s": N / (ms * 1e-3),
                              "collective": "NCCL all_to_all_single x1" if ws > 1 else "none",
                              "roundtrip_exact": ok, "scaling": "strong"}
+        # the same transform with the transpose as one peer-store kernel
+        # (gfp_exchange_transpose over CUDA IPC peer pointers) instead of
+        # pack / all_to_all_single / unpack
+        shp = ShardedFFT(ops, k, N1, N2, rank, ws, group).use_peer_exchange()
+        t = timed_loop(lambda: shp.forward(cols), steps, 2, ws, flush, stream)
+        ms = max_over_ranks(sum(t) / len(t), ws)
+        yc = shp.forward_columns(cols)
+        tx = timed_loop(lambda: shp.peer.transpose("rows", yc, A=shp.c2, B=N1), steps, 2, ws,
+                        flush, stream)
+        xms = max_over_ranks(sum(tx) / len(tx), ws)
+        xbytes = 2 * (N // ws) * k * 8  # read + write of this rank's block
+        del yc
+        rows = shp.forward(cols)
+        okp = bool((shp.inverse(rows).view(torch.int64) == cols.view(torch.int64)).all().item())
+        same = bool((rows.view(torch.int64) == sh.forward(cols).view(torch.int64)).all().item())
+        res["c4_sharded_peer"] = {"workload": "C4 fwd k=8 N=2^24 four-step 2^12 x 2^12, "
+                                              "peer-store exchange",
+                                  "n_gpus": ws, "ms_fwd": ms, "elements_per_s": N / (ms * 1e-3),
+                                  "collective": "gfp_exchange_transpose (CUDA IPC peer stores) "
+                                                "+ 2 host barriers" if ws > 1 else "none (local)",
+                                  "roundtrip_exact": okp, "equals_all_to_all_path": same,
+                                  "exchange_ms": xms,
+                                  "exchange_gbs_per_rank": xbytes / (xms * 1e-3) / 1e9,
+                                  "scaling": "strong"}
+        if shp.peer is not None:
+            shp.peer.close()
         del cols, rows
         torch.cuda.empty_cache()
     except Exception as exc:
-        res["c4_sharded"] = {"error": str(exc)[:300]}
+        res.setdefault("c4_sharded", {"error": str(exc)[:300]})
+        res["c4_sharded_peer"] = {"error": str(exc)[:300]}
     return res
 
 

@@ -174,6 +174,28 @@ int gfp_poly_mul_host2(gfp_fft_plan *plan, const uint64_t *f, int64_t nf, const 
 int gfp_fft_twiddle(const gfp_fft_plan *plan, const uint64_t *x, uint64_t *out, int64_t batch,
                     int64_t n, int64_t row0, int inverse, void *stream);
 
+/* The four-step transpose as direct stores into every rank's receive
+   buffer (the reference has no distributed transform --
+   this replaces the pack / all_to_all / unpack of the exchange that
+   sharded.py otherwise does with torch.distributed.all_to_all_single).
+   src is this rank's digit-major block [A][k][B]; dst[g] (g < world <= 16)
+   is rank g's receive buffer [B/world][k][world * A] -- a peer pointer from
+   gfp_ipc_open, or a local buffer -- and
+       dst[g][bl][d][rank * A + a] = src[a][d][g * (B/world) + bl].
+   One HBM/NVLink-bound kernel, stream-ordered; the caller separates it from
+   the peers' use of their buffers with a barrier.  GFP_EINVAL on bad sizes
+   (B % world != 0, world > 16, null pointers). */
+int gfp_exchange_transpose(const uint64_t *src, uint64_t *const *dst, int world, int rank,
+                           int64_t A, int k, int64_t B, void *stream);
+
+/* CUDA IPC for the exchange's peer pointers (one process per GPU):
+   gfp_ipc_get_handle writes the 64-byte handle of the allocation holding ptr
+   and ptr's byte offset in it; gfp_ipc_open maps a peer's handle and returns
+   the peer address (+ offset); gfp_ipc_close unmaps it. */
+int gfp_ipc_get_handle(const void *ptr, unsigned char *handle64, int64_t *offset);
+int gfp_ipc_open(const unsigned char *handle64, int64_t offset, void **ptr);
+int gfp_ipc_close(void *ptr, int64_t offset);
+
 /* Number of kernel launches issued by the last exec/poly_mul call on this
    plan (instrumentation for the benchmark's gpu_launches count). */
 int64_t gfp_fft_plan_last_launches(const gfp_fft_plan *plan);

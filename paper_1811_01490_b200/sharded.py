@@ -47,6 +47,18 @@ class ShardedFFT:
         self.rank, self.world, self.group = rank, world, group
         self.c1 = N1 // world  # local rows
         self.c2 = N2 // world  # local columns
+        self.peer = None       # PeerExchange: the transpose as peer stores
+
+    def exchange_shapes(self):
+        return {"rows": (self.c1, self.k, self.N2), "cols": (self.c2, self.k, self.N1)}
+
+    def use_peer_exchange(self, device=None, local_peers=None):
+        """Switch the transpose from all_to_all_single to gfp_exchange_transpose
+        (direct stores into every rank's receive buffer over CUDA IPC peer
+        pointers; one kernel instead of pack / all-to-all / unpack)."""
+        self.peer = PeerExchange(self.exchange_shapes(), self.rank, self.world, self.group,
+                                 device, local_peers)
+        return self
 
     # -- exchange ---------------------------------------------------------
     def _all_to_all(self, send):
@@ -59,40 +71,58 @@ class ShardedFFT:
         return recv.view(send.dtype) if send.dtype != recv.dtype else recv
 
     # -- forward ----------------------------------------------------------
+    def forward_columns(self, cols):
+        """Step 1 (+2): column DFTs [N2/G, k, N1] -> A[n2l, d, k1]."""
+        if getattr(self.ops, "fused", False):  # lazy digits through the exchange
+            return self.ops.fft_ex(cols, "N1", inverse=False, in_canon=True, out_canon=False)
+        y = self.ops.fft(cols, "N1", inverse=False)
+        return self.ops.twiddle(y, self.rank * self.c2, inverse=False)   # * w_N^(n2 k1)
+
+    def forward_rows(self, rows):
+        """Step 4: row DFTs [N1/G, k, N2] (+ the folded twiddle)."""
+        if getattr(self.ops, "fused", False):  # * w_N^(k1 n2) on the row DFT's first pass
+            return self.ops.fft_ex(_u64(rows), "N2", inverse=False, in_canon=False,
+                                   out_canon=True, ft_row0=self.rank * self.c1)
+        return self.ops.fft(_u64(rows), "N2", inverse=False)
+
     def forward(self, cols):
         """cols [N2/G, k, N1] (canonical) -> rows [N1/G, k, N2] (canonical)."""
         G, k, c1, c2 = self.world, self.k, self.c1, self.c2
-        fused = getattr(self.ops, "fused", False)
-        if fused:  # lazy digits through the exchange, twiddle folded into the row DFT
-            y = self.ops.fft_ex(cols, "N1", inverse=False, in_canon=True, out_canon=False)
+        y = self.forward_columns(cols)
+        if self.peer is not None:  # one kernel stores into every rank's row buffer
+            rows = self.peer.transpose("rows", y, A=c2, B=self.N1)
         else:
-            y = self.ops.fft(cols, "N1", inverse=False)               # A[n2l, d, k1]
-            y = self.ops.twiddle(y, self.rank * c2, inverse=False)    # * w_N^(n2 k1)
-        send = _i64(y).view(c2, k, G, c1).permute(2, 0, 1, 3).contiguous()
-        recv = self._all_to_all(send)                                  # [g, n2l, d, k1l]
-        rows = recv.permute(3, 2, 0, 1).reshape(c1, k, self.N2).contiguous()
-        if fused:  # * w_N^(k1 n2) on the row DFT's first pass
-            return self.ops.fft_ex(_u64(rows), "N2", inverse=False, in_canon=False,
-                                   out_canon=True, ft_row0=self.rank * c1)
-        return self.ops.fft(_u64(rows), "N2", inverse=False)
+            send = _i64(y).view(c2, k, G, c1).permute(2, 0, 1, 3).contiguous()
+            recv = self._all_to_all(send)                                  # [g, n2l, d, k1l]
+            rows = recv.permute(3, 2, 0, 1).reshape(c1, k, self.N2).contiguous()
+        return self.forward_rows(rows)
 
     # -- inverse ----------------------------------------------------------
+    def inverse_rows(self, rows):
+        """Inverse row DFTs [N1/G, k, N2] -> B[k1l, d, n2]."""
+        if getattr(self.ops, "fused", False):
+            return self.ops.fft_ex(rows, "N2", inverse=True, in_canon=True, out_canon=False)
+        return self.ops.fft(rows, "N2", inverse=True)
+
+    def inverse_columns(self, cols):
+        """Conjugate twiddle + inverse column DFTs [N2/G, k, N1]."""
+        if getattr(self.ops, "fused", False):  # * w_N^-(n2 k1) on the first pass
+            return self.ops.fft_ex(_u64(cols), "N1", inverse=True, in_canon=False,
+                                   out_canon=True, ft_row0=self.rank * self.c2, ft_inverse=True)
+        cols = self.ops.twiddle(_u64(cols), self.rank * self.c2, inverse=True)
+        return self.ops.fft(cols, "N1", inverse=True)
+
     def inverse(self, rows):
         """rows [N1/G, k, N2] -> cols [N2/G, k, N1]; inverse of forward()."""
         G, k, c1, c2 = self.world, self.k, self.c1, self.c2
-        fused = getattr(self.ops, "fused", False)
-        if fused:
-            z = self.ops.fft_ex(rows, "N2", inverse=True, in_canon=True, out_canon=False)
+        z = self.inverse_rows(rows)
+        if self.peer is not None:
+            cols = self.peer.transpose("cols", z, A=c1, B=self.N2)
         else:
-            z = self.ops.fft(rows, "N2", inverse=True)               # B[k1l, d, n2]
-        send = _i64(z).view(c1, k, G, c2).permute(2, 0, 1, 3).contiguous()
-        recv = self._all_to_all(send)                                  # [g, k1l, d, n2l]
-        cols = recv.permute(3, 2, 0, 1).reshape(c2, k, self.N1).contiguous()
-        if fused:  # * w_N^-(n2 k1) on the column inverse DFT's first pass
-            return self.ops.fft_ex(_u64(cols), "N1", inverse=True, in_canon=False,
-                                   out_canon=True, ft_row0=self.rank * c2, ft_inverse=True)
-        cols = self.ops.twiddle(_u64(cols), self.rank * c2, inverse=True)
-        return self.ops.fft(cols, "N1", inverse=True)
+            send = _i64(z).view(c1, k, G, c2).permute(2, 0, 1, 3).contiguous()
+            recv = self._all_to_all(send)                                  # [g, k1l, d, n2l]
+            cols = recv.permute(3, 2, 0, 1).reshape(c2, k, self.N1).contiguous()
+        return self.inverse_columns(cols)
 
     # -- global <-> local layouts (tests and benchmark data placement) ----
     def scatter_columns(self, x):
@@ -107,6 +137,99 @@ class ShardedFFT:
         k1 = torch.arange(self.rank * self.c1, (self.rank + 1) * self.c1).view(-1, 1)
         k2 = torch.arange(self.N2).view(1, -1)
         return k1 + self.N1 * k2
+
+
+def _barrier(group):
+    import torch.distributed as dist
+    torch.cuda.current_stream().synchronize()
+    dist.barrier(group=group)
+
+
+class PeerExchange:
+    """Receive buffers of the four-step transpose and every rank's address of
+    them: CUDA IPC handles (gfp_ipc_get_handle / gfp_ipc_open) gathered once
+    with all_gather_object, so each exchange is one gfp_exchange_transpose
+    launch writing over NVLink into the owners' buffers.  Two host barriers
+    bracket it: peers have finished reading their buffers (previous call)
+    before the stores start, and every store into this rank's buffer has
+    landed before it is read.
+
+    ``local_peers`` (tests, one process): a list of G PeerExchange-like
+    receive-buffer dicts on this device standing in for the peers (no
+    barriers; the caller runs the ranks' stages in order)."""
+
+    def __init__(self, shapes, rank, world, group=None, device=None, local_peers=None):
+        import ctypes
+        from . import _lib
+        self.rank, self.world, self.group = rank, world, group
+        self._opened = []
+        self.addrs = {}
+        self.local = local_peers is not None
+        if self.local:
+            self.recv = local_peers[rank]
+            for n in shapes:
+                self.addrs[n] = [p[n].data_ptr() for p in local_peers]
+            return
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.recv = {n: torch.empty(sh, dtype=torch.int64, device=dev).view(torch.uint64)
+                     for n, sh in shapes.items()}
+        if world == 1:
+            self.addrs = {n: [t.data_ptr()] for n, t in self.recv.items()}
+            return
+        import torch.distributed as dist
+        lib = _lib.load()
+        mine = {}
+        for n, t in self.recv.items():
+            h = ctypes.create_string_buffer(64)
+            off = ctypes.c_int64(0)
+            _lib.check(lib.gfp_ipc_get_handle(ctypes.c_void_p(t.data_ptr()), h,
+                                              ctypes.byref(off)), "gfp_ipc_get_handle")
+            mine[n] = (h.raw, off.value)
+        every = [None] * world
+        dist.all_gather_object(every, mine, group=group)
+        for n, t in self.recv.items():
+            addrs = []
+            for g in range(world):
+                if g == rank:
+                    addrs.append(t.data_ptr())
+                    continue
+                raw, off = every[g][n]
+                ptr = ctypes.c_void_p(0)
+                _lib.check(lib.gfp_ipc_open(raw, off, ctypes.byref(ptr)), "gfp_ipc_open")
+                addrs.append(ptr.value)
+                self._opened.append((ptr.value, off))
+            self.addrs[n] = addrs
+
+    @staticmethod
+    def local_buffers(shapes, world, device="cuda"):
+        """Receive buffers of `world` emulated ranks on one device."""
+        return [{n: torch.empty(sh, dtype=torch.int64, device=device).view(torch.uint64)
+                 for n, sh in shapes.items()} for _ in range(world)]
+
+    def transpose(self, name, src, A, B):
+        """src [A, k, B] -> every rank's recv[name] (see gfp_exchange_transpose);
+        returns this rank's receive buffer."""
+        import ctypes
+        from . import _lib
+        src = _u64(src).contiguous()
+        k = src.shape[1]
+        many = self.world > 1 and not self.local
+        if many:
+            _barrier(self.group)
+        ptrs = (ctypes.c_uint64 * self.world)(*self.addrs[name])
+        _lib.check(_lib.load().gfp_exchange_transpose(
+            ctypes.c_void_p(src.data_ptr()), ptrs, self.world, self.rank, A, k, B,
+            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), "gfp_exchange_transpose")
+        if many:
+            _barrier(self.group)
+        return self.recv[name]
+
+    def close(self):
+        import ctypes
+        from . import _lib
+        for ptr, off in self._opened:
+            _lib.load().gfp_ipc_close(ctypes.c_void_p(ptr), off)
+        self._opened = []
 
 
 class GpuShardOps:

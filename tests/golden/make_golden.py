@@ -267,6 +267,22 @@ def task_c3_idx0(_):
                        "seconds": time.time() - t0}
 
 
+def task_c3_idx63(_):
+    # the last transform of the C3 batch: draws [63 * 2^20, 64 * 2^20) of one
+    # Random(3) stream (bench_cli._fft_bench_setup convention, one stream)
+    N = 1 << 20
+    params, field, plan = field_plan(16, N)
+    rng = random.Random(3)
+    for _ in range(63 * N):
+        rng.randrange(params.p)
+    v = draws(params, 3, N, rng=rng)
+    t0 = time.time()
+    w = fft.dft_general(list(v), plan, field)
+    return "c3_idx63", {"k": 16, "N": N, "seed": 3, "batch_index": 63,
+                        "input": digest(v), "forward": digest(w),
+                        "seconds": time.time() - t0}
+
+
 def task_c4_prefix(_):
     N = 1 << 16
     params, field, plan = field_plan(8, N)
@@ -310,6 +326,22 @@ def task_c5(_):
                       "y": digest(ys), "products": digest(zs)}
 
 
+def task_c5_full(_):
+    # all 2^22 C5 pairs through the reference's gfp_mul_bigint (gfp_mult.py:504-512)
+    k = 32
+    params = GfpParams(DEFAULT_RADIX[k], k)
+    rng = random.Random(5)
+    n_pairs = 1 << 22
+    h = hashlib.sha256()
+    t0 = time.time()
+    for _ in range(n_pairs):
+        a, b = rng.randrange(params.p), rng.randrange(params.p)
+        z = gfp_mult.gfp_mul_bigint(params, gfp_encode(params, a), gfp_encode(params, b))
+        h.update(np.asarray(z, dtype=np.uint64).astype("<u8").tobytes())
+    return "c5_mul_full", {"k": k, "pairs": n_pairs, "seed": 5,
+                           "products": h.hexdigest()[:16], "seconds": time.time() - t0}
+
+
 def task_c5_fft(_):
     N = 1 << 18
     params, field, plan = field_plan(32, N)
@@ -349,8 +381,8 @@ def main():
              (32, 64), (64, 128)]
     tasks += [(task_roots, it) for it in roots]
     if args.big:
-        tasks = [(task_c4_full, None), (task_c3_idx0, None),
-                 (task_c5_fft, None)] + tasks
+        tasks = [(task_c4_full, None), (task_c3_idx0, None), (task_c3_idx63, None),
+                 (task_c5_full, None), (task_c5_fft, None)] + tasks
     if args.only:
         keep = set(args.only.split(","))
         tasks = [t for t in tasks if t[0].__name__ in keep]
