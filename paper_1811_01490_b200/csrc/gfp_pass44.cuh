@@ -35,6 +35,9 @@
 #ifndef P44_MINB
 #define P44_MINB 5  // CTAs per SM the NW = 4 variant is register-bounded for (96 regs)
 #endif
+#ifndef P44_SPLIT2
+#define P44_SPLIT2 1  // NW > 4: stage 2's outputs split over all NW warps (else 4 warps)
+#endif
 #ifndef P44_AUNROLL
 #define P44_AUNROLL 1  // phase-A elements interleaved per thread (experiment hook)
 #endif
@@ -398,13 +401,21 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
     }
     }
     __syncthreads();
-    if (w >= 4)
+    // Stage 2 over SPL = NW / 4 warps per u0 (P44_SPLIT2): every warp gathers
+    // its u0's four slots and computes the (cheap, lazy) 4-point DFT, then
+    // normalises / canonicalises / stores only its 4 / SPL outputs u1 -- the
+    // expensive per-output work spread over all NW warps instead of 4.
+    constexpr int SPL = (P44_SPLIT2 && NW > 4) ? NW / 4 : 1;
+    constexpr int NU = 4 / SPL;  // outputs per warp
+    if (SPL == 1 && w >= 4)
         return;
+    const int u0 = w & 3;
+    const int h = SPL == 1 ? 0 : w >> 2;  // output block u1 in [h NU, h NU + NU)
 
-    // ---- stage 2: u0 = w; gather Y[t1][u0], twiddle rho^(t1 u0), DFT over t1
+    // ---- stage 2: gather Y[t1][u0], twiddle rho^(t1 u0), DFT over t1
 #pragma unroll
     for (int t1 = 0; t1 < 4; t1++) {
-        const i64 *slot = sm + ((w * 4 + t1) * 32 + lane) * SLOT;
+        const i64 *slot = sm + ((u0 * 4 + t1) * 32 + lane) * SLOT;
 #pragma unroll
         for (int d = 0; d < KD; d += 2) {
             const longlong2 v = *reinterpret_cast<const longlong2 *>(slot + d);
@@ -412,51 +423,68 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
             e[t1][d + 1] = v.y;
         }
     }
-    switch (w) {
+    switch (u0) {
     case 0: p44::dft4<KD, INV, 0>(e[0], e[1], e[2], e[3]); break;
     case 1: p44::dft4<KD, INV, 1>(e[0], e[1], e[2], e[3]); break;
     case 2: p44::dft4<KD, INV, 2>(e[0], e[1], e[2], e[3]); break;
     default: p44::dft4<KD, INV, 3>(e[0], e[1], e[2], e[3]); break;
+    }
+    if (SPL > 1 && h > 0) {  // this warp's outputs into e[0 .. NU-1] (static indices)
+#pragma unroll
+        for (int q = 0; q < NU; q++) {
+#pragma unroll
+            for (int d = 0; d < KD; d++) {
+                i64 v = e[q][d];
+#pragma unroll
+                for (int hh = 1; hh < SPL; hh++)
+                    v = h == hh ? e[hh * NU + q][d] : v;
+                e[q][d] = v;
+            }
+        }
     }
     // one balanced normalisation per output, then (last pass) the canonical
     // form, once for all three store paths below (keeps the kernel's code
     // small: the store paths only move digits)
     const bool canon = A.canon || em_out;
 #pragma unroll
-    for (int u1 = 0; u1 < 4; u1++) {
-        p44::normalize_el<KD, SPARSE>(e[u1], rc);
+    for (int q = 0; q < NU; q++) {
+        p44::normalize_el<KD, SPARSE>(e[q], rc);
         if (canon) {
             u64 c[KD];
-            lazy_to_canonical_bf<KD>(e[u1], c, rc);
+            lazy_to_canonical_bf<KD>(e[q], c, rc);
 #pragma unroll
             for (int d = 0; d < KD; d++)
-                e[u1][d] = (i64)c[d];
+                e[q][d] = (i64)c[d];
         }
     }
     if (em_out) {
         // last pass (Ns = M: output u of group j at j + u M), element-major,
-        // possibly mapped host memory: park the canonical outputs in this
-        // warp's own stage-2 slots (rows 4 w + u1), then write each u's 32
-        // elements (2 KB contiguous) with lane-contiguous 16 B stores
+        // possibly mapped host memory: park the canonical outputs in the
+        // stage-2 slots (rows 4 u0 + u1), then write each u's 32 elements
+        // (2 KB contiguous) with lane-contiguous 16 B stores
+        if (SPL > 1)  // the u0 slots are read by every warp of the u0 above
+            asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
 #pragma unroll
-        for (int u1 = 0; u1 < 4; u1++) {
-            i64 *slot = sm + ((4 * w + u1) * 32 + lane) * SLOT;
+        for (int q = 0; q < NU; q++) {
+            const int u1 = h * NU + q;
+            i64 *slot = sm + ((4 * u0 + u1) * 32 + lane) * SLOT;
 #pragma unroll
             for (int d = 0; d < KD; d += 2)
-                *reinterpret_cast<longlong2 *>(slot + d) = make_longlong2(e[u1][d], e[u1][d + 1]);
+                *reinterpret_cast<longlong2 *>(slot + d) = make_longlong2(e[q][d], e[q][d + 1]);
         }
         __syncwarp();
 #pragma unroll
-        for (int u1 = 0; u1 < 4; u1++) {
-            const int64_t ubase = j0 + ((int64_t)(w + 4 * u1) << lM);
+        for (int q = 0; q < NU; q++) {
+            const int u1 = h * NU + q;
+            const int64_t ubase = j0 + ((int64_t)(u0 + 4 * u1) << lM);
             u64 *rowp = em_out + ubase * KD;
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-                const int e = (lane >> 2) + 8 * q, dp = (lane & 3) * 2;
+            for (int qq = 0; qq < 4; qq++) {
+                const int e = (lane >> 2) + 8 * qq, dp = (lane & 3) * 2;
                 const longlong2 v =
-                    *reinterpret_cast<const longlong2 *>(sm + ((4 * w + u1) * 32 + e) * SLOT + dp);
+                    *reinterpret_cast<const longlong2 *>(sm + ((4 * u0 + u1) * 32 + e) * SLOT + dp);
                 if (e < gpc && j0 + e < M && ubase + e < A.n_out)
-                    reinterpret_cast<ulonglong2 *>(rowp)[lane + 32 * q] =
+                    reinterpret_cast<ulonglong2 *>(rowp)[lane + 32 * qq] =
                         make_ulonglong2((u64)v.x, (u64)v.y);
             }
         }
@@ -468,21 +496,22 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
         // outputs digit-major ([d][g][u], row pitch 17: conflict-free both
         // ways) over the slots, then write each digit row's 512 consecutive
         // positions lane-contiguously.
+        constexpr int NT = SPL * 128;  // threads in stage 2
         i64 *park = sm;
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // stage-2 slot reads done
+        asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");  // stage-2 slot reads done
 #pragma unroll
-        for (int u1 = 0; u1 < 4; u1++) {
-            const int u = w + 4 * u1;
+        for (int q = 0; q < NU; q++) {
+            const int u = u0 + 4 * (h * NU + q);
 #pragma unroll
             for (int d = 0; d < KD; d++)
-                park[(d * 32 + lane) * 17 + u] = e[u1][d];
+                park[(d * 32 + lane) * 17 + u] = e[q][d];
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        const int tid = threadIdx.x;  // < 128: the four stage-2 warps
+        asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+        const int tid = threadIdx.x;  // < NT: the stage-2 warps
         u64 *obase = out + (j0 << 4);
 #pragma unroll
-        for (int q4 = 0; q4 < 4; q4++) {
-            const int q = tid + 128 * q4;      // position 16 j0 + q
+        for (int q4 = 0; q4 < 512 / NT; q4++) {
+            const int q = tid + NT * q4;       // position 16 j0 + q
             const int g = q >> 4, u = q & 15;  // group j0 + g, output u
             if (g < gpc && j0 + g < M) {
 #pragma unroll
@@ -497,11 +526,11 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
     // X[u0 + 4 u1] = e[u1] -> (j / Ns) Ns K + (j mod Ns) + u Ns
     const int64_t base = ((j >> lNs) << (lNs + 4)) + (j & nsmask);
 #pragma unroll
-    for (int u1 = 0; u1 < 4; u1++) {
-        const int64_t pos = base + ((int64_t)(w + 4 * u1) << lNs);
+    for (int q = 0; q < NU; q++) {
+        const int64_t pos = base + ((int64_t)(u0 + 4 * (h * NU + q)) << lNs);
 #pragma unroll
         for (int d = 0; d < KD; d++)
-            __stcs(out + ((int64_t)d << lN) + pos, (u64)e[u1][d]);
+            __stcs(out + ((int64_t)d << lN) + pos, (u64)e[q][d]);
     }
 }
 
