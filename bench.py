@@ -549,9 +549,10 @@ def multi_gpu_configs(args, ws, rank, dev, flush, stream):
                              "n_gpus": ws, "ms_fwd": ms, "elements_per_s": N / (ms * 1e-3),
                              "collective": "NCCL all_to_all_single x1" if ws > 1 else "none",
                              "roundtrip_exact": ok, "scaling": "strong"}
-        # the same transform with the transpose as one peer-store kernel
-        # (gfp_exchange_transpose over CUDA IPC peer pointers) instead of
-        # pack / all_to_all_single / unpack
+        # the same transform with the transpose as peer stores (CUDA IPC peer
+        # pointers) fused into the column DFTs' last pass
+        # (gfp_fft_exec_exchange) instead of pack / all_to_all_single / unpack;
+        # the standalone gfp_exchange_transpose kernel is timed beside it
         shp = ShardedFFT(ops, k, N1, N2, rank, ws, group).use_peer_exchange()
         t = timed_loop(lambda: shp.forward(cols), steps, 2, ws, flush, stream)
         ms = max_over_ranks(sum(t) / len(t), ws)
@@ -567,11 +568,13 @@ def multi_gpu_configs(args, ws, rank, dev, flush, stream):
         res["c4_sharded_peer"] = {"workload": "C4 fwd k=8 N=2^24 four-step 2^12 x 2^12, "
                                               "peer-store exchange",
                                   "n_gpus": ws, "ms_fwd": ms, "elements_per_s": N / (ms * 1e-3),
-                                  "collective": "gfp_exchange_transpose (CUDA IPC peer stores) "
-                                                "+ 2 host barriers" if ws > 1 else "none (local)",
+                                  "collective": "peer stores fused into the column DFTs' last "
+                                                "pass (gfp_fft_exec_exchange, CUDA IPC) + 2 host "
+                                                "barriers" if ws > 1 else
+                                                "none (the fused last pass stores locally)",
                                   "roundtrip_exact": okp, "equals_all_to_all_path": same,
-                                  "exchange_ms": xms,
-                                  "exchange_gbs_per_rank": xbytes / (xms * 1e-3) / 1e9,
+                                  "standalone_exchange_kernel_ms": xms,
+                                  "standalone_exchange_gbs_per_rank": xbytes / (xms * 1e-3) / 1e9,
                                   "scaling": "strong"}
         if shp.peer is not None:
             shp.peer.close()

@@ -188,6 +188,20 @@ int gfp_fft_twiddle(const gfp_fft_plan *plan, const uint64_t *x, uint64_t *out, 
 int gfp_exchange_transpose(const uint64_t *src, uint64_t *const *dst, int world, int rank,
                            int64_t A, int k, int64_t B, void *stream);
 
+/* gfp_fft_exec_ex (no four-step twiddle) whose LAST pass stores straight
+   into the exchange's receive buffers instead of an output vector: the
+   column DFTs of the sharded four-step fused with the transpose (SURVEY 8(e)
+   steps 2-4).  in is this rank's batch [batch][k][N]; element (b, i) of the
+   result lands in dst[g] (world ranks, g = i / (N/world)) at
+   [(i mod N/world)][d][rank * batch + b] -- gfp_exchange_transpose's layout
+   with A = batch, B = N.  scratch and work are two [batch][k][N] buffers.
+   GFP_EUNSUPPORTED unless k = 8 (the radix-16 pass kernel), e >= 2,
+   world <= 8 a power of two, batch % 4 == 0 (then use gfp_fft_exec_ex +
+   gfp_exchange_transpose). */
+int gfp_fft_exec_exchange(const gfp_fft_plan *plan, const uint64_t *in, uint64_t *scratch,
+                          uint64_t *work, int64_t batch, int inverse, int in_canon, int out_canon,
+                          uint64_t *const *dst, int world, int rank, void *stream);
+
 /* CUDA IPC for the exchange's peer pointers (one process per GPU):
    gfp_ipc_get_handle writes the 64-byte handle of the allocation holding ptr
    and ptr's byte offset in it; gfp_ipc_open maps a peer's handle and returns

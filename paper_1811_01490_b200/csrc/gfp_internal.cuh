@@ -58,6 +58,13 @@ struct PassArgs {
     const u64 *ft_lh;
     int ft_lN, ft_lM, ft_inv, ft_root_inv;
     int64_t ft_row0;
+    // four-step exchange fused into the last pass (k_pass44, PassIO::xdst):
+    // element (b, pos) of this rank's batch goes to rank g = pos >> lxb at
+    //   xdst[g] + ((pos & (2^lxb - 1)) k + d) xg xA + xrank xA + b
+    // (gfp_exchange_transpose's layout); xg = 0: off
+    u64 *xdst[8];
+    int xg, xrank, lxb;
+    int64_t xA;
 };
 
 // Extras of one transform's first / last pass (k_pass44 only):
@@ -74,6 +81,10 @@ struct PassIO {
     const gfp_fft_plan *ft;
     int64_t ft_row0;
     int ft_inv;
+    // the last pass stores into the four-step exchange's receive buffers
+    // (xg ranks, up to 8) instead of `out`
+    u64 *const *xdst;
+    int xg, xrank;
 };
 
 // ---------------------------------------------------------------------------

@@ -436,6 +436,10 @@ static inline int make_pass_args(const gfp_fft_plan *p, const u64 *in, u64 *out,
     A.ft_lh = nullptr;
     A.ft_lN = A.ft_lM = A.ft_inv = A.ft_root_inv = 0;
     A.ft_row0 = 0;
+    A.xg = A.xrank = A.lxb = 0;
+    A.xA = 0;
+    for (int g = 0; g < 8; g++)
+        A.xdst[g] = nullptr;
     if (em) {
         if (Ns == 1 && em->ft && (scale || in_canon))
             return GFP_EUNSUPPORTED;  // first pass with N^-1 or canonical input
@@ -456,6 +460,16 @@ static inline int make_pass_args(const gfp_fft_plan *p, const u64 *in, u64 *out,
         if (canon && em->out) {
             A.out_em = em->out;
             A.n_out = em->n_out;
+        }
+        if (em->xg && Ns * p->K == p->N) {  // last pass: stores go to the exchange
+            if (Ns == 1 || em->xg > 8 || (em->xg & (em->xg - 1)) || batch % 4 || in2 || pre)
+                return GFP_EUNSUPPORTED;
+            A.xg = em->xg;
+            A.xrank = em->xrank;
+            A.lxb = ilog2_exact(p->N / em->xg);
+            A.xA = batch;
+            for (int g = 0; g < em->xg; g++)
+                A.xdst[g] = em->xdst[g];
         }
     }
     return GFP_OK;
@@ -490,7 +504,7 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
         return err;
     if (launch_pass44<KD>(A, p->M, in2 ? 2 * batch : batch, st))
         return cuda_status();
-    if (A.in_em || A.out_em || A.ft_lh)
+    if (A.in_em || A.out_em || A.ft_lh || A.xg)
         return GFP_EUNSUPPORTED;
     dim3 grid((unsigned)((p->M + G - 1) / G), (unsigned)(in2 ? 2 * batch : batch));
     if constexpr (P2Radix<KD>::a != 0) {

@@ -170,8 +170,9 @@ GFP_D void normalize_el(i64 (&v)[KD], const RadixConsts &rc)
 
 }  // namespace p44
 
-template <int KD, int SPARSE, bool INV, int NW>
-__global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1) k_pass44(PassArgs A)
+template <int KD, int SPARSE, bool INV, int NW, bool XCH = false>
+__global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? 4 : P44_MINB) : NW == 8 ? 2 : 1)
+    k_pass44(PassArgs A)
 {
     static_assert(KD == 8, "radix 4 x 4 pass is for K = 16");
     constexpr int K = 2 * KD;
@@ -180,7 +181,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;  // t1 in stage 1, u0 in stage 2 (warp-uniform)
 
-    int64_t bidx = blockIdx.y;
+    // fused four-step exchange (last pass, A.xg ranks): a CTA spans 4
+    // transforms x 8 groups (lane = 8 ts + jl) so the transposed stores
+    // (consecutive transforms adjacent) fill whole 32 B sectors
+    constexpr bool xch = XCH;  // A.xg != 0 (a separate instantiation: lane-dependent
+                               // batch pointers cost registers)
+    int64_t bidx = xch ? (int64_t)blockIdx.y * 4 + (lane >> 3) : blockIdx.y;
     const u64 *in_base = A.in;
     u64 *out_base = A.out;
     const u64 *em_in = A.in_em;
@@ -206,8 +212,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
     // over every SM: launch_pass44)
     const int gpc = A.gpc;
     const int64_t j0 = (int64_t)blockIdx.x * gpc;
-    const int64_t j = j0 + lane;
-    const bool active = lane < gpc && j < M;
+    const int64_t j = j0 + (xch ? (lane & 7) : lane);
+    const bool active = (xch || lane < gpc) && j < M;
 
     // programmatic dependent launch: let the next pass's CTAs be scheduled
     // as this grid drains, and wait for the previous pass's writes before the
@@ -525,6 +531,25 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44_MINB : NW == 8 ? 2 : 1)
         return;
     // X[u0 + 4 u1] = e[u1] -> (j / Ns) Ns K + (j mod Ns) + u Ns
     const int64_t base = ((j >> lNs) << (lNs + 4)) + (j & nsmask);
+    if (xch) {  // straight into the owner's receive buffer (peer pointer or local)
+        const int64_t GA = (int64_t)A.xg * A.xA;
+        const int64_t col = (int64_t)A.xrank * A.xA + bidx;
+        const int64_t bmask = ((int64_t)1 << A.lxb) - 1;
+#pragma unroll
+        for (int q = 0; q < NU; q++) {
+            const int64_t pos = base + ((int64_t)(u0 + 4 * (h * NU + q)) << lNs);
+            const int g = (int)(pos >> A.lxb);
+            u64 *dp = A.xdst[0];
+#pragma unroll
+            for (int gg = 1; gg < 8; gg++)
+                dp = g == gg ? A.xdst[gg] : dp;
+            dp += (pos & bmask) * KD * GA + col;
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                __stcs(dp + d * GA, (u64)e[q][d]);
+        }
+        return;
+    }
 #pragma unroll
     for (int q = 0; q < NU; q++) {
         const int64_t pos = base + ((int64_t)(u0 + 4 * (h * NU + q)) << lNs);
@@ -574,17 +599,17 @@ static inline void launch_pdl(void (*kern)(PassArgs), dim3 grid, int threads, cu
 }
 
 // NW <= 8: dynamic shared memory for the cp.async staging rows ([NW][k][32])
-template <int KD, int SP, bool IV, int NW>
+template <int KD, int SP, bool IV, int NW, bool XCH = false>
 static inline void launch_p44(dim3 grid, cudaStream_t st, const PassArgs &A)
 {
     const size_t smem = NW >= P44_PF_MINNW ? (size_t)NW * KD * 32 * sizeof(u64) : 0;
     static bool set = false;
     if (!set) {
-        cudaFuncSetAttribute(k_pass44<KD, SP, IV, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        cudaFuncSetAttribute(k_pass44<KD, SP, IV, NW, XCH>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         set = true;
     }
-    launch_pdl(k_pass44<KD, SP, IV, NW>, grid, NW * 32, st, A, smem);
+    launch_pdl(k_pass44<KD, SP, IV, NW, XCH>, grid, NW * 32, st, A, smem);
 }
 
 // launcher: returns 1 when it handled the pass
@@ -619,10 +644,16 @@ static int launch_pass44(const PassArgs &A0, int64_t M, int64_t nsets, cudaStrea
         if (gpc_env >= 1 && gpc_env <= 32)
             gpc = gpc_env;
         PassArgs A = A0;
+        if (A.xg)  // fused exchange: 8 groups x 4 transforms per CTA
+            gpc = 8;
         A.gpc = gpc;
-        dim3 grid((unsigned)((M + gpc - 1) / gpc), (unsigned)nsets);
+        dim3 grid((unsigned)((M + gpc - 1) / gpc), (unsigned)(A.xg ? nsets / 4 : nsets));
         const bool inv = A.rot_inv != 0;
 #define P44_LAUNCH(SP, IV)                                                                    \
+    if (A.xg) {                                                                               \
+        launch_p44<KD, SP, IV, 4, true>(grid, st, A);                                         \
+        return 1;                                                                             \
+    }                                                                                         \
     switch (nw) {                                                                             \
     case 4: launch_p44<KD, SP, IV, 4>(grid, st, A); break;                                     \
     case 8: launch_p44<KD, SP, IV, 8>(grid, st, A); break;                                     \

@@ -187,7 +187,8 @@ static int run_transform2(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, c
         int pass = 0;
         while (pass < e) {
             const bool em_first = em && pass == 0 && (em->in || em->ft);
-            const bool em_last = em && pass + 1 == e - 1 && em->out && out_canon;
+            const bool em_last =
+                em && pass + 1 == e - 1 && ((em->out && out_canon) || em->xg);
             const bool pair = pass + 1 < e && !em_first && !em_last && p->k == 8 &&
                               pass256_ok(p) && !(pass == 0 && pre && inverse && pass + 1 == e - 1);
             span[nl++] = pair ? 2 : 1;
@@ -232,8 +233,8 @@ static int run_transform2(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, c
             Ns *= p->K;
         pass += span[l];
     }
-    if (em && em->out && out_canon)
-        return cuda_status();  // the last pass wrote the element-major output
+    if (em && ((em->out && out_canon) || em->xg))
+        return cuda_status();  // the last pass wrote the element-major output / the exchange
     if (src != out)
         cudaMemcpyAsync(out, src, sizeof(u64) * (size_t)p->k * p->N * batch,
                         cudaMemcpyDeviceToDevice, st);
@@ -480,6 +481,26 @@ int gfp_fft_exec_ex(const gfp_fft_plan *cp, const uint64_t *in, uint64_t *out, u
     PassIO io = {nullptr, nullptr, 0, 0, nullptr, 0, ft, ft_row0, ft_inverse ? 1 : 0};
     return run_transform(p, in, out, work, nullptr, batch, inverse ? 1 : 0, in_canon ? 1 : 0,
                          out_canon ? 1 : 0, (cudaStream_t)stream, ft ? &io : nullptr);
+}
+
+int gfp_fft_exec_exchange(const gfp_fft_plan *cp, const uint64_t *in, uint64_t *scratch,
+                          uint64_t *work, int64_t batch, int inverse, int in_canon, int out_canon,
+                          uint64_t *const *dst, int world, int rank, void *stream)
+{
+    gfp_fft_plan *p = const_cast<gfp_fft_plan *>(cp);
+    if (!p || !in || !scratch || !work || !dst || batch < 1 || world < 1 || rank < 0 ||
+        rank >= world || p->N % world)
+        return GFP_EINVAL;
+    for (int g = 0; g < world; g++)
+        if (!dst[g])
+            return GFP_EINVAL;
+    if (p->k != 8 || p->e < 2 || world > 8 || (world & (world - 1)) || batch % 4 ||
+        !em_io_supported(p))
+        return GFP_EUNSUPPORTED;
+    p->last_launches = 0;
+    PassIO io = {nullptr, nullptr, 0, 0, nullptr, 0, nullptr, 0, 0, dst, world, rank};
+    return run_transform(p, in, scratch, work, nullptr, batch, inverse ? 1 : 0, in_canon ? 1 : 0,
+                         out_canon ? 1 : 0, (cudaStream_t)stream, &io);
 }
 
 int gfp_poly_mul(const gfp_fft_plan *cp, const uint64_t *f, const uint64_t *g, uint64_t *out,

@@ -52,12 +52,15 @@ class ShardedFFT:
     def exchange_shapes(self):
         return {"rows": (self.c1, self.k, self.N2), "cols": (self.c2, self.k, self.N1)}
 
-    def use_peer_exchange(self, device=None, local_peers=None):
-        """Switch the transpose from all_to_all_single to gfp_exchange_transpose
-        (direct stores into every rank's receive buffer over CUDA IPC peer
-        pointers; one kernel instead of pack / all-to-all / unpack)."""
+    def use_peer_exchange(self, device=None, local_peers=None, fuse=True):
+        """Switch the transpose from all_to_all_single to direct stores into
+        every rank's receive buffer over CUDA IPC peer pointers: fused into
+        the last pass of the preceding DFTs (gfp_fft_exec_exchange) when
+        `fuse` and the pass kernel supports it, else one
+        gfp_exchange_transpose kernel (instead of pack / all-to-all / unpack)."""
         self.peer = PeerExchange(self.exchange_shapes(), self.rank, self.world, self.group,
                                  device, local_peers)
+        self.peer.fuse = fuse
         return self
 
     # -- exchange ---------------------------------------------------------
@@ -85,17 +88,28 @@ class ShardedFFT:
                                    out_canon=True, ft_row0=self.rank * self.c1)
         return self.ops.fft(_u64(rows), "N2", inverse=False)
 
+    def columns_to_rows(self, cols):
+        """Steps 1-3: column DFTs, twiddle and the transpose; returns this
+        rank's rows [N1/G, k, N2] (before the row DFTs)."""
+        G, k, c1, c2 = self.world, self.k, self.c1, self.c2
+        if self.peer is not None:
+            if self.peer.fuse and getattr(self.ops, "fused", False):
+                # the column DFTs' last pass stores straight into the owners'
+                # row buffers (gfp_fft_exec_exchange)
+                if self.peer.bracket(lambda: self.ops.fft_exchange(
+                        cols, "N1", False, True, False, self.peer.addrs["rows"],
+                        G, self.rank)):
+                    return self.peer.recv["rows"]
+            y = self.forward_columns(cols)  # one kernel stores into every rank's buffer
+            return self.peer.transpose("rows", y, A=c2, B=self.N1)
+        y = self.forward_columns(cols)
+        send = _i64(y).view(c2, k, G, c1).permute(2, 0, 1, 3).contiguous()
+        recv = self._all_to_all(send)                                  # [g, n2l, d, k1l]
+        return recv.permute(3, 2, 0, 1).reshape(c1, k, self.N2).contiguous()
+
     def forward(self, cols):
         """cols [N2/G, k, N1] (canonical) -> rows [N1/G, k, N2] (canonical)."""
-        G, k, c1, c2 = self.world, self.k, self.c1, self.c2
-        y = self.forward_columns(cols)
-        if self.peer is not None:  # one kernel stores into every rank's row buffer
-            rows = self.peer.transpose("rows", y, A=c2, B=self.N1)
-        else:
-            send = _i64(y).view(c2, k, G, c1).permute(2, 0, 1, 3).contiguous()
-            recv = self._all_to_all(send)                                  # [g, n2l, d, k1l]
-            rows = recv.permute(3, 2, 0, 1).reshape(c1, k, self.N2).contiguous()
-        return self.forward_rows(rows)
+        return self.forward_rows(self.columns_to_rows(cols))
 
     # -- inverse ----------------------------------------------------------
     def inverse_rows(self, rows):
@@ -112,17 +126,26 @@ class ShardedFFT:
         cols = self.ops.twiddle(_u64(cols), self.rank * self.c2, inverse=True)
         return self.ops.fft(cols, "N1", inverse=True)
 
+    def rows_to_columns(self, rows):
+        """Inverse row DFTs and the transpose back; returns this rank's
+        columns [N2/G, k, N1] (before the conjugate twiddle)."""
+        G, k, c1, c2 = self.world, self.k, self.c1, self.c2
+        if self.peer is not None:
+            if self.peer.fuse and getattr(self.ops, "fused", False):
+                if self.peer.bracket(lambda: self.ops.fft_exchange(
+                        rows, "N2", True, True, False, self.peer.addrs["cols"],
+                        G, self.rank)):
+                    return self.peer.recv["cols"]
+            z = self.inverse_rows(rows)
+            return self.peer.transpose("cols", z, A=c1, B=self.N2)
+        z = self.inverse_rows(rows)
+        send = _i64(z).view(c1, k, G, c2).permute(2, 0, 1, 3).contiguous()
+        recv = self._all_to_all(send)                                  # [g, k1l, d, n2l]
+        return recv.permute(3, 2, 0, 1).reshape(c2, k, self.N1).contiguous()
+
     def inverse(self, rows):
         """rows [N1/G, k, N2] -> cols [N2/G, k, N1]; inverse of forward()."""
-        G, k, c1, c2 = self.world, self.k, self.c1, self.c2
-        z = self.inverse_rows(rows)
-        if self.peer is not None:
-            cols = self.peer.transpose("cols", z, A=c1, B=self.N2)
-        else:
-            send = _i64(z).view(c1, k, G, c2).permute(2, 0, 1, 3).contiguous()
-            recv = self._all_to_all(send)                                  # [g, k1l, d, n2l]
-            cols = recv.permute(3, 2, 0, 1).reshape(c2, k, self.N1).contiguous()
-        return self.inverse_columns(cols)
+        return self.inverse_columns(self.rows_to_columns(rows))
 
     # -- global <-> local layouts (tests and benchmark data placement) ----
     def scatter_columns(self, x):
@@ -164,6 +187,7 @@ class PeerExchange:
         self.rank, self.world, self.group = rank, world, group
         self._opened = []
         self.addrs = {}
+        self.fuse = True
         self.local = local_peers is not None
         if self.local:
             self.recv = local_peers[rank]
@@ -206,6 +230,18 @@ class PeerExchange:
         return [{n: torch.empty(sh, dtype=torch.int64, device=device).view(torch.uint64)
                  for n, sh in shapes.items()} for _ in range(world)]
 
+    def bracket(self, fn):
+        """Run fn (stores into the peers' buffers) between the two barriers;
+        returns fn's result.  Every rank takes the same branch (the
+        supported-or-not outcome of fn depends only on shapes)."""
+        many = self.world > 1 and not self.local
+        if many:
+            _barrier(self.group)
+        res = fn()
+        if many and res is not False:
+            _barrier(self.group)
+        return res
+
     def transpose(self, name, src, A, B):
         """src [A, k, B] -> every rank's recv[name] (see gfp_exchange_transpose);
         returns this rank's receive buffer."""
@@ -213,15 +249,14 @@ class PeerExchange:
         from . import _lib
         src = _u64(src).contiguous()
         k = src.shape[1]
-        many = self.world > 1 and not self.local
-        if many:
-            _barrier(self.group)
         ptrs = (ctypes.c_uint64 * self.world)(*self.addrs[name])
-        _lib.check(_lib.load().gfp_exchange_transpose(
-            ctypes.c_void_p(src.data_ptr()), ptrs, self.world, self.rank, A, k, B,
-            ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)), "gfp_exchange_transpose")
-        if many:
-            _barrier(self.group)
+
+        def run():
+            _lib.check(_lib.load().gfp_exchange_transpose(
+                ctypes.c_void_p(src.data_ptr()), ptrs, self.world, self.rank, A, k, B,
+                ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                "gfp_exchange_transpose")
+        self.bracket(run)
         return self.recv[name]
 
     def close(self):
@@ -278,6 +313,30 @@ class GpuShardOps:
             ft_row0 if ft_row0 is not None else 0, 1 if ft_inverse else 0,
             vp(torch.cuda.current_stream().cuda_stream)), "gfp_fft_exec_ex")
         return out
+
+    def fft_exchange(self, x, which, inverse, in_canon, out_canon, dst_addrs, world, rank):
+        """Batched transform whose last pass stores into the exchange buffers
+        dst_addrs (gfp_fft_exec_exchange); False when the pass kernel cannot
+        (the caller then transposes with gfp_exchange_transpose)."""
+        import ctypes
+        from . import _lib
+        lib = _lib.load()
+        x = x.contiguous()
+        plan = self.plans[which]
+        B = x.shape[0]
+        scratch = torch.empty_like(x)
+        work = torch.empty(int(lib.gfp_fft_workspace_words(plan.handle, B)),
+                           dtype=torch.uint64, device=x.device)
+        vp = ctypes.c_void_p
+        ptrs = (ctypes.c_uint64 * world)(*dst_addrs)
+        code = lib.gfp_fft_exec_exchange(
+            plan.handle, vp(x.data_ptr()), vp(scratch.data_ptr()), vp(work.data_ptr()), B,
+            1 if inverse else 0, 1 if in_canon else 0, 1 if out_canon else 0, ptrs, world, rank,
+            vp(torch.cuda.current_stream().cuda_stream))
+        if code == _lib.GFP_EUNSUPPORTED:
+            return False
+        _lib.check(code, "gfp_fft_exec_exchange")
+        return True
 
     def twiddle(self, x, row0, inverse):
         import ctypes
