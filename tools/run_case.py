@@ -17,6 +17,22 @@ from bench import R, WORKLOADS  # noqa: E402
 def main():
     key = sys.argv[1] if len(sys.argv) > 1 else "c4"
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    if key == "c4s":  # sharded C4 (1 rank): fused exchange, then the standalone kernel
+        from paper_1811_01490_b200.sharded import GpuShardOps, ShardedFFT
+        N1 = N2 = 1 << 12
+        params = gp.GfpParams(R[8], 8)
+        field = gp.GfpFftField(params, backend="cuda")
+        ops = GpuShardOps(field, 16, N1, N2, gp.roots_for(params, N1 * N2))
+        sh = ShardedFFT(ops, 8, N1, N2).use_peer_exchange()
+        cols = gp.vec.uniform(N1, params, seed=400, batch=N2)
+        for _ in range(reps):
+            sh.forward(cols)
+        y = sh.forward_columns(cols)
+        for _ in range(reps):
+            sh.peer.transpose("rows", y, A=N2, B=N1)
+        torch.cuda.synchronize()
+        print("ok", key, reps)
+        return
     wl = WORKLOADS[key]
     k, K, e, B = wl["k"], wl["K"], wl["e"], wl["batch"]
     if key == "c3" and len(sys.argv) > 3:
