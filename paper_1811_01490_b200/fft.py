@@ -173,6 +173,8 @@ def fft(x, plan, inverse=False, out=None):
     else:
         vec._require_cuda(out)
         out = out.view_as(xb)
+    if B == 0:  # an empty batch: nothing to transform
+        return out
     work = torch.empty(int(_lib.load().gfp_fft_workspace_words(plan.handle, B)),
                        dtype=torch.uint64, device=x.device)
     _lib.check(_lib.load().gfp_fft_exec(plan.handle, _ptr(xb), _ptr(out), _ptr(work), B,

@@ -146,3 +146,80 @@ def test_sharded_single_rank_layouts():
     want = ops.big.forward(x)
     got = _np(rows).transpose(0, 2, 1).reshape(-1, k)
     assert np.array_equal(got, want[sh.gather_rows_index().numpy().reshape(-1)])
+
+
+class GlooPeer:
+    """CPU stand-in for sharded.PeerExchange: the same receive buffers and
+    the same store layout as gfp_exchange_transpose,
+        dst_g[bl][d][rank A + a] = src[a][d][g b + bl],
+    realised with a gloo all_to_all, so the peer-exchange branches of
+    ShardedFFT (columns_to_rows / rows_to_columns) run as two real ranks.
+    The kernel itself is checked against this layout on the GPU
+    (test_exchange_transpose_layout)."""
+
+    def __init__(self, shapes, rank, world):
+        self.rank, self.world, self.fuse = rank, world, True
+        self.recv = {n: torch.empty(sh, dtype=torch.int64) for n, sh in shapes.items()}
+        self.barriers = 0
+
+    def bracket(self, fn):
+        dist.barrier()
+        res = fn()
+        if res is not False:
+            dist.barrier()
+        self.barriers += 1
+        return res
+
+    def transpose(self, name, src, A, B):
+        G, b = self.world, B // self.world
+        s = src.view(torch.int64) if src.dtype != torch.int64 else src
+        kk = s.shape[1]
+
+        def run():
+            send = s.view(A, kk, G, b).permute(2, 0, 1, 3).contiguous()   # [g][a][d][bl]
+            got = torch.empty_like(send)
+            dist.all_to_all_single(got, send)                             # [src rank][a][d][bl]
+            self.recv[name].view(b, kk, G, A)[:] = got.permute(3, 2, 0, 1)
+        self.bracket(run)
+        return self.recv[name]
+
+
+def _peer_worker(rank, world, port, N1, N2, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1811_01490_b200.sharded import ShardedFFT
+        N = N1 * N2
+        _, omega = O.gfp_root(k, R8, N)
+        ops = OracleShardOps(N1, N2, omega)
+        sh = ShardedFFT(ops, k, N1, N2, rank, world)
+        sh.peer = GlooPeer(sh.exchange_shapes(), rank, world)
+        x = O.random_elements(5, k, R8, N)
+        xd = torch.from_numpy(np.ascontiguousarray(x.T).view(np.int64))
+        cols = sh.scatter_columns(xd)
+        rows = sh.forward(cols)
+        want = ops.big.forward(x)
+        idx = sh.gather_rows_index().numpy()
+        ok_fwd = np.array_equal(_np(rows).transpose(0, 2, 1).reshape(-1, k),
+                                want[idx.reshape(-1)])
+        ok_inv = np.array_equal(_np(sh.inverse(rows)), _np(cols))
+        q.put((rank, bool(ok_fwd), bool(ok_inv), sh.peer.barriers))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_peer_exchange_two_ranks_gloo():
+    # the peer-store exchange branches of ShardedFFT with two gloo ranks:
+    # one bracketed transpose per direction, results equal the oracle DFT
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, 16, 256, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    res = sorted(q.get(timeout=5) for _ in range(2))
+    assert all(p.exitcode == 0 for p in procs)
+    assert res == [(0, True, True, 2), (1, True, True, 2)]
