@@ -168,8 +168,11 @@ def dist_setup():
     if ws > 1:
         import torch.distributed as dist
         backend = "nccl" if torch.cuda.is_available() else "gloo"
+        # GFP_BENCH_BACKEND=gloo: a flow smoke test of the multi-rank path with
+        # more ranks than GPUs (ranks share devices; its timings mean nothing)
+        backend = os.environ.get("GFP_BENCH_BACKEND", backend)
         if torch.cuda.is_available():
-            torch.cuda.set_device(local)
+            torch.cuda.set_device(local % torch.cuda.device_count())
         dist.init_process_group(backend=backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
@@ -328,7 +331,7 @@ def run_ours(args, ws, rank, local):
     import torch
     import paper_1811_01490_b200 as gp
     from paper_1811_01490_b200 import _lib
-    dev = torch.device("cuda", local if ws > 1 else 0)
+    dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.current_stream()
     flush_buf = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > L2
 
@@ -380,7 +383,7 @@ def run_ours(args, ws, rank, local):
     def step():
         graph.replay()
 
-    sampler = ClockSampler(local if ws > 1 else 0)
+    sampler = ClockSampler(torch.cuda.current_device())
     sampler.start()
     times = timed_loop(step, args.steps, args.warmup, ws, flush, stream)
     clocks = sampler.stop()
