@@ -196,7 +196,7 @@ int gfp_exchange_transpose(const uint64_t *src, uint64_t *const *dst, int world,
    [(i mod N/world)][d][rank * batch + b] -- gfp_exchange_transpose's layout
    with A = batch, B = N.  scratch and work are two [batch][k][N] buffers.
    GFP_EUNSUPPORTED unless k = 8 (the radix-16 pass kernel), e >= 2,
-   world <= 8 a power of two, batch % 4 == 0 (then use gfp_fft_exec_ex +
+   world <= 8 a power of two, batch % 8 == 0 (then use gfp_fft_exec_ex +
    gfp_exchange_transpose). */
 int gfp_fft_exec_exchange(const gfp_fft_plan *plan, const uint64_t *in, uint64_t *scratch,
                           uint64_t *work, int64_t batch, int inverse, int in_canon, int out_canon,

@@ -462,7 +462,7 @@ static inline int make_pass_args(const gfp_fft_plan *p, const u64 *in, u64 *out,
             A.n_out = em->n_out;
         }
         if (em->xg && Ns * p->K == p->N) {  // last pass: stores go to the exchange
-            if (Ns == 1 || em->xg > 8 || (em->xg & (em->xg - 1)) || batch % 4 || in2 || pre)
+            if (Ns == 1 || em->xg > 8 || (em->xg & (em->xg - 1)) || batch % 8 || in2 || pre)
                 return GFP_EUNSUPPORTED;
             A.xg = em->xg;
             A.xrank = em->xrank;

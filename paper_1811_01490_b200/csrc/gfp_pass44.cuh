@@ -41,6 +41,10 @@
 #ifndef P44_L2PF
 #define P44_L2PF 0  // NW = 4: bulk L2 prefetch of the next element's rows (measured: C4 5.07 -> 5.31 ms, off)
 #endif
+#ifndef P44_XT
+#define P44_XT 8  // transforms per CTA in the fused-exchange pass: 8 -> 64 B store segments
+                  // (measured at 1 GPU: sharded C4 5.237 ms with 4, 5.218 ms with 8)
+#endif
 #ifndef P44_AUNROLL
 #define P44_AUNROLL 1  // phase-A elements interleaved per thread (experiment hook)
 #endif
@@ -184,12 +188,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? 4 : P44_MINB) : NW =
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;  // t1 in stage 1, u0 in stage 2 (warp-uniform)
 
-    // fused four-step exchange (last pass, A.xg ranks): a CTA spans 4
-    // transforms x 8 groups (lane = 8 ts + jl) so the transposed stores
+    // fused four-step exchange (last pass, A.xg ranks): a CTA spans P44_XT
+    // transforms x 32/P44_XT groups (lane = (32/P44_XT) ts + jl) so the transposed stores
     // (consecutive transforms adjacent) fill whole 32 B sectors
     constexpr bool xch = XCH;  // A.xg != 0 (a separate instantiation: lane-dependent
                                // batch pointers cost registers)
-    int64_t bidx = xch ? (int64_t)blockIdx.y * 4 + (lane >> 3) : blockIdx.y;
+    int64_t bidx = xch ? (int64_t)blockIdx.y * P44_XT + lane / (32 / P44_XT) : blockIdx.y;
     const u64 *in_base = A.in;
     u64 *out_base = A.out;
     const u64 *em_in = A.in_em;
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? 4 : P44_MINB) : NW =
     // over every SM: launch_pass44)
     const int gpc = A.gpc;
     const int64_t j0 = (int64_t)blockIdx.x * gpc;
-    const int64_t j = j0 + (xch ? (lane & 7) : lane);
+    const int64_t j = j0 + (xch ? (lane & (32 / P44_XT - 1)) : lane);
     const bool active = (xch || lane < gpc) && j < M;
 
     // programmatic dependent launch: let the next pass's CTAs be scheduled
@@ -667,9 +671,9 @@ static int launch_pass44(const PassArgs &A0, int64_t M, int64_t nsets, cudaStrea
             gpc = gpc_env;
         PassArgs A = A0;
         if (A.xg)  // fused exchange: 8 groups x 4 transforms per CTA
-            gpc = 8;
+            gpc = 32 / P44_XT;
         A.gpc = gpc;
-        dim3 grid((unsigned)((M + gpc - 1) / gpc), (unsigned)(A.xg ? nsets / 4 : nsets));
+        dim3 grid((unsigned)((M + gpc - 1) / gpc), (unsigned)(A.xg ? nsets / P44_XT : nsets));
         const bool inv = A.rot_inv != 0;
 #define P44_LAUNCH(SP, IV)                                                                    \
     if (A.xg) {                                                                               \

@@ -494,7 +494,7 @@ int gfp_fft_exec_exchange(const gfp_fft_plan *cp, const uint64_t *in, uint64_t *
     for (int g = 0; g < world; g++)
         if (!dst[g])
             return GFP_EINVAL;
-    if (p->k != 8 || p->e < 2 || world > 8 || (world & (world - 1)) || batch % 4 ||
+    if (p->k != 8 || p->e < 2 || world > 8 || (world & (world - 1)) || batch % 8 ||
         !em_io_supported(p))
         return GFP_EUNSUPPORTED;
     p->last_launches = 0;
