@@ -51,3 +51,15 @@ def test_invalid_arguments_rejected_before_device_work():
     om = (ctypes.c_uint64 * 8)()
     assert lib.gfp_fft_plan_create(ctypes.byref(h), 8, 10, 12, 2, om, None) == _lib.GFP_EINVAL
     assert lib.gfp_fft_plan_create(ctypes.byref(h), 8, 10, 32, 2, om, None) == _lib.GFP_EINVAL
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    # no CPU fallback: importing the package without its CUDA library raises
+    import subprocess
+    import sys
+    env = dict(os.environ, GFPFFT_LIB=str(tmp_path / "missing" / "libgfpfft.so"))
+    code = "import paper_1811_01490_b200"
+    p = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert p.returncode != 0
+    assert "ImportError" in p.stderr and "no CPU fallback" in p.stderr
