@@ -635,6 +635,14 @@ def extra_configs(args, dev, flush, stream):
                              tera_imad_per_s=n * 4 * k * k / (ms * 1e-3) / 1e12,
                              tera_imad_executed_per_s=n * 3 * k * k / (ms * 1e-3) / 1e12)
 
+                # the same products through the reference's mechanism
+                # (gfp_vec_mul_crt: word-prime convolutions + CRT + LHC)
+                def cstep():
+                    gp.vec.mul_crt(a, b, params)
+                t = timed_loop(cstep, max(3, steps // 2), 2, 1, flush, stream)
+                ms = sum(t) / len(t)
+                entry.update(ms_mul_mechanism=ms, mechanism_muls_per_s=n / (ms * 1e-3))
+
                 def step():
                     gp.fft_tensor(x, plan, out=y)
                 t = timed_loop(step, steps, 2, 1, flush, stream)

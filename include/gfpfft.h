@@ -80,6 +80,16 @@ int gfp_vec_mul_pow_r(const uint64_t *x, uint64_t *z, int64_t n, int k, uint64_t
 int gfp_vec_mul(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z, int64_t n,
                 int k, uint64_t r, void *stream);
 
+/* z = x * y mod p through the reference's own mechanism (gfp_mul_fft,
+   gfp_mult.py:416-501, paper Alg. 13): negacyclic convolutions of the digit
+   vectors over the word primes P1, P2 (theta-weighted NTTs in Montgomery
+   form), CRT to signed coefficients, LHC split, carry normalisation.  The
+   same canonical product as gfp_vec_mul (which the transforms use);
+   GFP_ECONFIG when check_prime_compat fails (gfp_mult.py:207-226),
+   GFP_EUNSUPPORTED for k > 64.  y_inc as in gfp_vec_mul. */
+int gfp_vec_mul_crt(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z, int64_t n,
+                    int k, uint64_t r, void *stream);
+
 /* z = x^e mod p, e given as little-endian host uint64 limbs shared by all
    elements.  Replaces gfp_pow (gfp_field.py:164-177) /
    GfpFftField.pow (gfp_mult.py:552-554). */

@@ -35,6 +35,7 @@ SIGNATURES = {
     "gfp_vec_sub": (_int, [_u64p, _u64p, _u64p, _i64, _int, _u64, _vp]),
     "gfp_vec_mul_pow_r": (_int, [_u64p, _u64p, _i64, _int, _u64, _int, _vp]),
     "gfp_vec_mul": (_int, [_u64p, _u64p, _i64, _u64p, _i64, _int, _u64, _vp]),
+    "gfp_vec_mul_crt": (_int, [_u64p, _u64p, _i64, _u64p, _i64, _int, _u64, _vp]),
     "gfp_vec_pow": (_int, [_u64p, ctypes.POINTER(ctypes.c_uint64), _int, _u64p, _i64, _int,
                            _u64, _vp]),
     "gfp_vec_is_canonical": (_int, [_u64p, _vp, _i64, _int, _u64, _vp]),

@@ -97,13 +97,15 @@ def _require_compat(params, crt):
     _compat_ok[key] = True
 
 
-def _mul_device(params, x, y, profile=None):
+def _mul_device(params, x, y, profile=None, mechanism=False):
     if len(x) != params.k or len(y) != params.k:
         raise ValueError("element must have k digits")
     t0 = time.perf_counter() if profile is not None else 0
     a = vec.to_device([x], params.k)
     b = vec.to_device([y], params.k)
-    z = vec.mul(a, b, params)
+    # mechanism: the reference's two-prime convolution + CRT + LHC route
+    # (gfp_vec_mul_crt); else the direct exact multiply the transforms use
+    z = vec.mul_crt(a, b, params) if mechanism and params.k <= 64 else vec.mul(a, b, params)
     out = vec.to_tuples(z)[0]
     if profile is not None:
         profile["device_mul"] = profile.get("device_mul", 0.0) + time.perf_counter() - t0
@@ -114,7 +116,7 @@ def gfp_mul_fft(params, crt, x, y, profile=None):
     """x * y mod p; raises ConfigurationError like the reference when the
     prime pair cannot carry k r^2 (gfp_mult.py:416-422)."""
     _require_compat(params, crt)
-    return _mul_device(params, x, y, profile)
+    return _mul_device(params, x, y, profile, mechanism=True)
 
 
 def gfp_mul_bigint(params, x, y):

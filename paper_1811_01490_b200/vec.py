@@ -92,6 +92,22 @@ def mul(x, y, params):
     return z
 
 
+def mul_crt(x, y, params):
+    """Element-wise product through the reference's own mechanism (two word-
+    prime negacyclic convolutions, CRT, LHC: gfp_mul_fft, gfp_mult.py:416-501);
+    the same canonical result as mul().  ConfigurationError when
+    check_prime_compat fails."""
+    _require_cuda(x, y)
+    z = torch.empty_like(x)
+    k, n = x.shape
+    y_inc = 0 if y.shape[1] == 1 and n != 1 else 1
+    if y_inc and y.shape != x.shape:
+        raise ValueError("shape mismatch")
+    _lib.check(_lib.load().gfp_vec_mul_crt(_ptr(x), _ptr(y), y_inc, _ptr(z), n, k, params.r,
+                                          _stream()), "gfp_vec_mul_crt")
+    return z
+
+
 def pow(x, e, params):
     """x^e for a non-negative Python int exponent shared by all elements."""
     _require_cuda(x)
