@@ -69,3 +69,30 @@ def test_compat_report():
     assert not rep.passed and rep.slack < 0
     ok = gp.check_prime_compat(gp.GfpParams(R8, 8), gp.crt_default())
     assert ok.passed and ok.slack > 0
+
+
+def test_oracle_element_ops_property():
+    # the CPU oracle's digit algorithms (gfp_field.py:82-161, gfp_mult.py)
+    # against plain integer arithmetic mod p for random (k, r) and operands
+    # (form B, zero and r - 1 digits included); the oracle is the checker of
+    # every GPU parity test, so it is itself checked here beyond the goldens
+    import numpy as np
+    from oracle import oracle as O
+    rng = random.Random(20261020)
+    for _ in range(40):
+        k = rng.choice([1, 2, 4, 8, 16, 32])
+        r = rng.choice([2, 3, rng.randrange(2, 1 << 16), rng.randrange(1 << 40, 1 << 62),
+                        rng.randrange(1 << 62, 1 << 64)])
+        params = gp.GfpParams(r, k)
+        p = params.p
+        vals = [0, 1, p - 1, p - 2, r, r - 1] + [rng.randrange(p) for _ in range(10)]
+        xs = [rng.choice(vals) for _ in range(24)]
+        ys = [rng.choice(vals) for _ in range(24)]
+        X = np.array([gp.gfp_encode(params, v) for v in xs], dtype=np.uint64)
+        Y = np.array([gp.gfp_encode(params, v) for v in ys], dtype=np.uint64)
+        dec = lambda A: [gp.gfp_decode(params, tuple(int(d) for d in row)) for row in A]  # noqa: E731
+        assert dec(O.add(X, Y, r)) == [(a + b) % p for a, b in zip(xs, ys)]
+        assert dec(O.sub(X, Y, r)) == [(a - b) % p for a, b in zip(xs, ys)]
+        assert dec(O.mul(X, Y, r, backend="school")) == [a * b % p for a, b in zip(xs, ys)]
+        i = rng.randrange(2 * k + 1)
+        assert dec(O.mul_pow_r(X, r, i)) == [a * pow(r, i, p) % p for a in xs]
