@@ -45,6 +45,9 @@
 #define P44_XT 8  // transforms per CTA in the fused-exchange pass: 8 -> 64 B store segments
                   // (measured at 1 GPU: sharded C4 5.237 ms with 4, 5.218 ms with 8)
 #endif
+#ifndef P44_MINB16
+#define P44_MINB16 1  // CTAs per SM the NW = 16 variant is register-bounded for
+#endif
 #ifndef P44_XCH_MINB
 #define P44_XCH_MINB 4  // CTAs/SM bound of the XCH variant (5: 96 regs + 220 B spills, sharded C4 5.19 -> 5.43 ms)
 #endif
@@ -181,7 +184,7 @@ GFP_D void normalize_el(i64 (&v)[KD], const RadixConsts &rc)
 }  // namespace p44
 
 template <int KD, int SPARSE, bool INV, int NW, bool XCH = false>
-__global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_MINB) : NW == 8 ? 2 : 1)
+__global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_MINB) : NW == 8 ? 2 : P44_MINB16)
     k_pass44(PassArgs A)
 {
     static_assert(KD == 8, "radix 4 x 4 pass is for K = 16");
