@@ -579,6 +579,27 @@ def multi_gpu_configs(args, ws, rank, dev, flush, stream):
                                   "standalone_exchange_kernel_ms": xms,
                                   "standalone_exchange_gbs_per_rank": xbytes / (xms * 1e-3) / 1e9,
                                   "scaling": "strong"}
+        if ws > 1:
+            try:
+                # the same with stream-ordered NCCL barriers instead of host ones
+                # (no host blocking between the column and row DFTs)
+                shp.peer.use_device_barrier()
+                if shp.peer.device_barrier:
+                    t = timed_loop(lambda: shp.forward(cols), steps, 2, ws, flush, stream)
+                    ms = max_over_ranks(sum(t) / len(t), ws)
+                    rows = shp.forward(cols)
+                    okd = bool((shp.inverse(rows).view(torch.int64)
+                                == cols.view(torch.int64)).all().item())
+                    samed = bool((rows.view(torch.int64)
+                                  == sh.forward(cols).view(torch.int64)).all().item())
+                    res["c4_sharded_peer_devsync"] = {
+                        "workload": "C4 fwd k=8 N=2^24 four-step, peer-store exchange, "
+                                    "stream-ordered NCCL barriers",
+                        "n_gpus": ws, "ms_fwd": ms, "elements_per_s": N / (ms * 1e-3),
+                        "roundtrip_exact": okd, "equals_all_to_all_path": samed,
+                        "scaling": "strong"}
+            except Exception as exc:
+                res["c4_sharded_peer_devsync"] = {"error": str(exc)[:300]}
         if shp.peer is not None:
             shp.peer.close()
         del cols, rows

@@ -188,6 +188,8 @@ class PeerExchange:
         self._opened = []
         self.addrs = {}
         self.fuse = True
+        self.device_barrier = False  # opt-in: use_device_barrier()
+        self._flag = None
         self.local = local_peers is not None
         if self.local:
             self.recv = local_peers[rank]
@@ -224,11 +226,32 @@ class PeerExchange:
                 self._opened.append((ptr.value, off))
             self.addrs[n] = addrs
 
+    def use_device_barrier(self):
+        """Replace the two host barriers by stream-ordered NCCL barriers (only
+        with an NCCL group; a no-op otherwise)."""
+        if self.world > 1 and not self.local:
+            import torch.distributed as dist
+            if dist.get_backend(self.group) == "nccl":
+                self.device_barrier = True
+                self._flag = torch.zeros(1, dtype=torch.int32,
+                                         device=next(iter(self.recv.values())).device)
+        return self
+
     @staticmethod
     def local_buffers(shapes, world, device="cuda"):
         """Receive buffers of `world` emulated ranks on one device."""
         return [{n: torch.empty(sh, dtype=torch.int64, device=device).view(torch.uint64)
                  for n, sh in shapes.items()} for _ in range(world)]
+
+    def _sync(self):
+        if self.device_barrier:
+            # stream-ordered barrier: a one-element NCCL all-reduce on the
+            # current stream (it starts after this rank's queued kernels and
+            # completes when every rank reached it; the host never blocks)
+            import torch.distributed as dist
+            dist.all_reduce(self._flag, group=self.group)
+        else:
+            _barrier(self.group)
 
     def bracket(self, fn):
         """Run fn (stores into the peers' buffers) between the two barriers;
@@ -236,10 +259,10 @@ class PeerExchange:
         supported-or-not outcome of fn depends only on shapes)."""
         many = self.world > 1 and not self.local
         if many:
-            _barrier(self.group)
+            self._sync()
         res = fn()
         if many and res is not False:
-            _barrier(self.group)
+            self._sync()
         return res
 
     def transpose(self, name, src, A, B):
