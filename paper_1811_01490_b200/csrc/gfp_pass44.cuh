@@ -51,6 +51,9 @@
 #ifndef P44_XCH_MINB
 #define P44_XCH_MINB 4  // CTAs/SM bound of the XCH variant (5: 96 regs + 220 B spills, sharded C4 5.19 -> 5.43 ms)
 #endif
+#ifndef P44_FAST0
+#define P44_FAST0 0  // NW = 4 multiply-free first pass, all loads issued first (measured C4 5.036 -> 5.062 ms: off)
+#endif
 #ifndef P44_AUNROLL
 #define P44_AUNROLL 1  // phase-A elements interleaved per thread (experiment hook)
 #endif
@@ -277,8 +280,35 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
         }
     };
     i64 e[4][KD];
+    // First pass with nothing to multiply (no twiddle at Ns = 1, no pointwise
+    // operand, no N^-1, no four-step twiddle), NW = 4: an HBM-bound stream.
+    // Issue all 16/NW elements' digit loads before parking any, so each
+    // thread has 4 x k loads in flight instead of k.
+    const bool fast0 = P44_FAST0 && NW == 4 && !xch && lNs == 0 && !pre && !A.scale &&
+                       !A.ft_lh && !em_in;
+    if (fast0) {
+        constexpr int EPT = 16 / NW;
+        i64 xa[EPT][KD];
+        const unsigned rowN = 1u << lN;
+#pragma unroll
+        for (int i = 0; i < EPT; i++) {
+            const u64 *src = in + j + ((int64_t)(w + NW * i) << lM);
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                xa[i][d] = active ? (i64)__ldcs(src + (unsigned)d * rowN) : 0;
+        }
+#pragma unroll
+        for (int i = 0; i < EPT; i++) {
+            if (A.in_canon && active)
+                to_balanced<KD>(xa[i], rc.r);
+            i64 *slot = sm + ((w + NW * i) * 32 + lane) * SLOT;
+#pragma unroll
+            for (int d = 0; d < KD; d += 2)
+                *reinterpret_cast<longlong2 *>(slot + d) = make_longlong2(xa[i][d], xa[i][d + 1]);
+        }
+    }
     P44_UNROLL(P44_AUNROLL)
-    for (int i = 0; i < 16 / NW; i++) {
+    for (int i = 0; i < (fast0 ? 0 : 16 / NW); i++) {
         const int t = w + NW * i;
         if (l2pf && i + 1 < 16 / NW)
             l2_prefetch(i + 1);
