@@ -60,35 +60,31 @@ def log(*a):
 # ---------------------------------------------------------------------------
 # algorithmic work model (counts what the kernels are asked to compute)
 
-def mults_per_transform(N, K, inverse=False, pre=False):
-    """General Z/pZ multiplies one transform performs: per Stockham pass,
-    element (j, t) is multiplied when its twiddle omega^E has a non-unit
-    omega^b part (E mod N/K != 0), every element on the inverse's last pass
-    (N^-1 folded in), and every element of pass 0 when a pointwise operand
-    is fused in."""
+def mults_in_pass(N, K, p, inverse=False, pre=False):
+    """General Z/pZ multiplies of Stockham pass p of one transform: element
+    (j, t) is multiplied when its twiddle omega^E has a non-unit omega^b part
+    (E mod N/K != 0), every element on the inverse's last pass (N^-1 folded
+    in), and every element of pass 0 when a pointwise operand is fused in."""
+    from math import gcd
     M = N // K
-    e = 0
-    n = N
-    while n > 1:
-        n //= K
-        e += 1
+    e = passes(N, K)
+    Ns = K ** p
     total = 0
-    Ns = 1
-    for p in range(e):
-        last = p == e - 1
-        if inverse and last:
-            total += N
-        elif Ns > 1:
-            # count (j, t), j < M, t < K with t * (j mod Ns) * (M / Ns) != 0 mod M
-            # <=> t * (j mod Ns) != 0 mod Ns; for fixed t exactly gcd(t, Ns)
-            # residues j mod Ns give 0
-            from math import gcd
-            per_block = sum(Ns - gcd(t, Ns) for t in range(K))
-            total += per_block * (M // Ns)
-        if pre and p == 0:
-            total += N
-        Ns *= K
+    if inverse and p == e - 1:
+        total += N
+    elif Ns > 1:
+        # count (j, t), j < M, t < K with t * (j mod Ns) * (M / Ns) != 0 mod M
+        # <=> t * (j mod Ns) != 0 mod Ns; for fixed t exactly gcd(t, Ns)
+        # residues j mod Ns give 0
+        total += sum(Ns - gcd(t, Ns) for t in range(K)) * (M // Ns)
+    if pre and p == 0:
+        total += N
     return total
+
+
+def mults_per_transform(N, K, inverse=False, pre=False):
+    """General Z/pZ multiplies one transform performs (all its passes)."""
+    return sum(mults_in_pass(N, K, p, inverse, pre) for p in range(passes(N, K)))
 
 
 def passes(N, K):
@@ -222,11 +218,54 @@ def cpu_poly_mul_rate(budget_s, threads):
     return N / per, per, len(times)
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_variants(budget_s):
+    """SURVEY 8(d)'s CPU plan on the C2 workload: both oracle backends (fft =
+    the reference's gfp-fft mechanism, school = its gfp-bigint route as a
+    schoolbook product), on 1 core and on every core."""
+    import numpy as np
+    from oracle import oracle as O
+    k, K, e = 8, 16, 4
+    N = K ** e
+    r = R[k]
+    _, w = O.gfp_root(k, r, N)
+    f = np.zeros((N, k), dtype=np.uint64)
+    g = f.copy()
+    f[: N // 2] = O.random_elements(1, k, r, N // 2)
+    g[: N // 2] = O.random_elements(2, k, r, N // 2)
+    out = []
+    cores = os.cpu_count() or 1
+    for backend in ("fft", "school"):
+        plan = O.Plan(k, r, K, e, w, backend=backend)
+        plan.prepare_inverse()
+        for th in sorted({1, cores}):
+            times = []
+            t_end = time.perf_counter() + budget_s
+            while not times or time.perf_counter() < t_end:
+                t0 = time.perf_counter()
+                prod = plan.poly_mul(f, g, threads=th)
+                times.append(time.perf_counter() - t0)
+            if O.digest(prod) != "ad746dbbdda033dd":
+                raise SystemExit("CPU baseline lost parity (%s)" % backend)
+            per = statistics.median(times)
+            out.append({"backend": backend, "cores": th, "value": N / per,
+                        "unit": "elements/s", "s_per_poly_mul": per, "runs": len(times)})
+    return out
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return
     from oracle import oracle as O
-    threads = O.lib().orc_max_threads() if hasattr(O.lib(), "orc_max_threads") else 1
     threads = max(1, os.cpu_count() or 1)
     wl = WORKLOADS["c2"]
     k, K, e = wl["k"], wl["K"], wl["e"]
@@ -268,6 +307,61 @@ def run_reference(args, ws, rank):
 # ---------------------------------------------------------------------------
 # our arm
 
+_GOLDEN = None
+
+
+def checked_roots(gp, params, N):
+    """roots_for (the reference's _gfp_root convention, bench_cli.py:398-402)
+    asserted against the root the reference itself produced for this (k, N)
+    (tests/golden/golden.json) before any timing."""
+    global _GOLDEN
+    omega = gp.roots_for(params, N)
+    if _GOLDEN is None:
+        try:
+            _GOLDEN = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
+        except (OSError, ValueError):
+            _GOLDEN = {}
+    g = _GOLDEN.get("root_k%d_N%d" % (params.k, N))
+    if g is not None and omega != tuple(int(d) for d in g["omega"]):
+        raise SystemExit("root for k=%d N=%d differs from the reference's" % (params.k, N))
+    return omega
+
+
+def pass_roofline(gp, plan, fn, k, N, K, batch, kind, hbm_peak, imad_peak, reps=5):
+    """Per-pass device times of fn() (CUDA events around each pass launch,
+    gfp_fft_plan_pass_times; median of reps) with each pass's algorithmic
+    HBM bytes (2 x 8k per element read + written, + 8k for a fused pointwise
+    operand) and algorithmic IMAD.WIDE (4k^2 per general multiply, SURVEY
+    8(d)); frac against the measured HBM copy peak for the multiply-free
+    pass and against the live IMAD.WIDE peak for the multiply passes."""
+    from paper_1811_01490_b200 import fft as F
+    fn()
+    runs = [F.pass_times(plan, fn)[1] for _ in range(reps)]
+    e = passes(N, K)
+    out = []
+    for i, (p, _) in enumerate(runs[0]):
+        ms = statistics.median(r[i][1] for r in runs)
+        if kind == "polymul":
+            inverse, first_inv = i >= e, i == e
+            sets = 2 if i < e else 1
+            pre = first_inv
+        else:
+            inverse, pre, sets = kind == "inv", False, 1
+        elems = batch * sets * N
+        nbytes = elems * 2 * 8 * k + (batch * N * 8 * k if pre else 0)
+        mults = batch * sets * mults_in_pass(N, K, p, inverse, pre)
+        imad = mults * 4 * k * k
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        timad = imad / (ms * 1e-3)
+        entry = {"launch": i, "pass": p, "inverse": inverse, "ms": ms, "hbm_bytes": nbytes,
+                 "gbs": gbs, "hbm_frac": gbs / hbm_peak, "general_mults": mults,
+                 "tera_imad_per_s": timad / 1e12, "imad_frac": timad / imad_peak,
+                 "bound": "hbm" if mults == 0 else "int"}
+        entry["frac"] = entry["hbm_frac"] if mults == 0 else entry["imad_frac"]
+        out.append(entry)
+    return out
+
+
 def probe_int_peak():
     from paper_1811_01490_b200 import _lib
     import torch
@@ -293,7 +387,7 @@ def setup_c2():
     N = K ** e
     params = gp.GfpParams(R[k], k)
     field = gp.GfpFftField(params, backend="cuda")
-    omega = gp.roots_for(params, N)
+    omega = checked_roots(gp, params, N)
     plan = gp.build_plan(field, K, e, omega)
     # synthetic inputs with the reference's distribution: the low half of
     # each operand uniform residues, the high half zero (degree 2^15 - 1)
@@ -409,6 +503,8 @@ def run_ours(args, ws, rank, local):
     except (OSError, ValueError):
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    # per-pass device times of one (stream-launched) poly-multiply
+    c2_passes = pass_roofline(gp, plan, direct, k, N, K, 1, "polymul", hbm_peak, peak_imad)
     traffic = None
     try:  # ncu --set full of the step's pass launches (tools/gpu_bench_profile.sh)
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -462,7 +558,10 @@ def run_ours(args, ws, rank, local):
                                           "Karatsuba): the integer-pipe utilisation"},
                      "traffic": traffic,
                      "traffic_note": "dram read+write bytes per step, ncu --set full over the "
-                                     "step's pass launches (profiles/ncu_traffic.json)",
+                                     "step's pass launches, from the committed capture "
+                                     "profiles/ncu_traffic.json (not this run)",
+                     "regime": "latency-bound, L2-resident (4 MiB operands; one wave of "
+                               "256 CTAs per pass)",
                      "algorithmic": "%d general multiplies x 4k^2 = %d IMAD.WIDE.U32 per step "
                                     "(SURVEY 8(d): schoolbook 32-bit limb products; executed "
                                     "3k^2 = %d)" % (mults, imad_alg, imad),
@@ -479,6 +578,10 @@ def run_ours(args, ws, rank, local):
                 "api": "gfp_poly_mul_host2 (C-ABI; pinned element-major host coefficient "
                        "arrays of the two degree-2^15-1 operands, read / product written "
                        "by the first / last transform pass over PCIe)"},
+        "passes": {"workload": "C2 poly-mul, one stream-launched step, per pass launch "
+                               "(forward passes transform both operands)",
+                   "hbm_peak_gbs": hbm_peak, "imad_peak_tera": peak_imad / 1e12,
+                   "launches": c2_passes},
         "gpu_launches": launches_per_step * args.steps,
         "gpu_launches_per_step": launches_per_step,
         "e2e_gpu_launches_per_step": e2e_launches,
@@ -491,14 +594,16 @@ def run_ours(args, ws, rank, local):
             line["cpu_baseline"] = {
                 "value": v, "unit": "elements/s", "cores": threads, "kind": "port",
                 "sample": "%d full C2 poly-muls (%.3f s each), oracle/gfp_oracle.c "
-                          "(gfp_mul_fft + dft_general restated), OpenMP" % (n, per)}
+                          "(gfp_mul_fft + dft_general restated), OpenMP" % (n, per),
+                "cpu_model": cpu_model(),
+                "variants": cpu_variants(args.cpu_budget / 4)}
         except Exception as exc:  # the oracle is optional on exotic hosts
             line["cpu_baseline"] = {"value": None, "error": str(exc)[:200]}
     multi = {}
     if not args.no_extra:
         multi = multi_gpu_configs(args, ws, rank, dev, flush, stream)
     if rank == 0 and not args.no_extra:
-        line["configs"] = extra_configs(args, dev, flush, stream)
+        line["configs"] = extra_configs(args, dev, flush, stream, hbm_peak, peak_imad)
         line["configs"].update(multi)
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -522,7 +627,7 @@ def multi_gpu_configs(args, ws, rank, dev, flush, stream):
         B = 64 // ws
         params = gp.GfpParams(R[k], k)
         plan = gp.build_plan(gp.GfpFftField(params, backend="cuda"), K, e,
-                             gp.roots_for(params, N))
+                             checked_roots(gp, params, N))
         x = gp.vec.uniform(N, params, seed=300 + rank, batch=B)
         y = torch.empty_like(x)
         t = timed_loop(lambda: gp.fft_tensor(x, plan, out=y), steps, 2, ws, flush, stream)
@@ -540,7 +645,7 @@ def multi_gpu_configs(args, ws, rank, dev, flush, stream):
         N = N1 * N2
         params = gp.GfpParams(R[k], k)
         field = gp.GfpFftField(params, backend="cuda")
-        ops = GpuShardOps(field, K, N1, N2, gp.roots_for(params, N))
+        ops = GpuShardOps(field, K, N1, N2, checked_roots(gp, params, N))
         group = None
         sh = ShardedFFT(ops, k, N1, N2, rank, ws, group)
         cols = gp.vec.uniform(N1, params, seed=400 + rank, batch=N2 // ws)
@@ -610,7 +715,7 @@ def multi_gpu_configs(args, ws, rank, dev, flush, stream):
     return res
 
 
-def extra_configs(args, dev, flush, stream):
+def extra_configs(args, dev, flush, stream, hbm_peak, imad_peak):
     """The other BASELINE.json configs, timed briefly (elements/s)."""
     import torch
     import paper_1811_01490_b200 as gp
@@ -623,7 +728,7 @@ def extra_configs(args, dev, flush, stream):
             N = K ** e
             params = gp.GfpParams(R[k], k)
             field = gp.GfpFftField(params, backend="cuda")
-            plan = gp.build_plan(field, K, e, gp.roots_for(params, N))
+            plan = gp.build_plan(field, K, e, checked_roots(gp, params, N))
             x = gp.vec.uniform(N, params, seed=7, batch=B if B > 1 else None)
             y = torch.empty_like(x)
             entry = {"workload": wl["name"]}
@@ -643,6 +748,8 @@ def extra_configs(args, dev, flush, stream):
                 entry.update(ms_fwd=ms, elements_per_s=B * N / (ms * 1e-3),
                              tera_imad_per_s=mults * 4 * k * k / (ms * 1e-3) / 1e12,
                              tera_imad_executed_per_s=mults * 3 * k * k / (ms * 1e-3) / 1e12)
+                entry["passes"] = pass_roofline(gp, plan, step, k, N, K, B, "fwd", hbm_peak,
+                                                imad_peak, reps=3)
             else:
                 n = 1 << 22
                 a = gp.vec.uniform(n, params, seed=51)

@@ -90,6 +90,17 @@ int gfp_vec_mul(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z
 int gfp_vec_mul_crt(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z, int64_t n,
                     int k, uint64_t r, void *stream);
 
+/* gfp_vec_mul_crt with the reference's per-step profile (gfp_mul_fft's
+   profile= keys, gfp_mult.py:428-500; bench_cli cmd_profile_mul,
+   bench_cli.py:470-494): step_cycles[0..5] (host) receive the SM cycles the
+   threads spent in convert_in, convolution, convert_out, crt, lhc and final
+   (summed over threads), *ms the kernel's device time.  A separate
+   instrumented kernel (clock64 around each step); same product.
+   Synchronous. */
+int gfp_vec_mul_crt_profile(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z,
+                            int64_t n, int k, uint64_t r, uint64_t *step_cycles, float *ms,
+                            void *stream);
+
 /* z = x^e mod p, e given as little-endian host uint64 limbs shared by all
    elements.  Replaces gfp_pow (gfp_field.py:164-177) /
    GfpFftField.pow (gfp_mult.py:552-554). */
@@ -223,6 +234,28 @@ int gfp_ipc_close(void *ptr, int64_t offset);
 /* Number of kernel launches issued by the last exec/poly_mul call on this
    plan (instrumentation for the benchmark's gpu_launches count). */
 int64_t gfp_fft_plan_last_launches(const gfp_fft_plan *plan);
+
+/* Capabilities of a plan's pass kernels (bit flags): GFP_CAP_EM_IO -- the
+   first / last pass read / write element-major (host) buffers themselves
+   (zero-copy host I/O); GFP_CAP_FT -- gfp_fft_exec_ex can fold a four-step
+   twiddle into the first pass; GFP_CAP_XCH -- gfp_fft_exec_exchange can
+   store the last pass into peer buffers.  Plans without a flag take the
+   staged / separate-kernel route for that feature. */
+#define GFP_CAP_EM_IO 1
+#define GFP_CAP_FT 2
+#define GFP_CAP_XCH 4
+int gfp_fft_plan_caps(const gfp_fft_plan *plan);
+
+/* Per-pass device timing.  With timing on, every later call on the plan
+   records CUDA events on its stream around each pass launch (the reference's
+   dft_general(profile=) phase accounting, fft.py:298-360, and the
+   benchmark's per-pass roofline); gfp_fft_plan_pass_times synchronises on
+   the last event and writes up to `max` per-launch durations (ms) with the
+   pass index of each launch within its transform (0 = the multiply-free
+   first pass of a forward transform), returning the count (negative
+   GFP_E* on failure).  Off by default: no events, no overhead. */
+int gfp_fft_plan_set_timing(gfp_fft_plan *plan, int on);
+int gfp_fft_plan_pass_times(gfp_fft_plan *plan, float *ms, int *pass, int max);
 
 /* Instrumentation: run `iters` x 8 independent IMAD.WIDE (32x32 -> 64)
    product chains per thread on a blocks x threads grid and report the kernel time and the

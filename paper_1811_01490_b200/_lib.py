@@ -18,6 +18,9 @@ GFP_ECONFIG = 2
 GFP_ECUDA = 3
 GFP_ENOMEM = 4
 GFP_EUNSUPPORTED = 5
+GFP_CAP_EM_IO = 1
+GFP_CAP_FT = 2
+GFP_CAP_XCH = 4
 
 # every symbol include/gfpfft.h declares: (name, restype, argtypes)
 _u64p = ctypes.c_void_p  # device or host pointers are passed as integers
@@ -36,6 +39,9 @@ SIGNATURES = {
     "gfp_vec_mul_pow_r": (_int, [_u64p, _u64p, _i64, _int, _u64, _int, _vp]),
     "gfp_vec_mul": (_int, [_u64p, _u64p, _i64, _u64p, _i64, _int, _u64, _vp]),
     "gfp_vec_mul_crt": (_int, [_u64p, _u64p, _i64, _u64p, _i64, _int, _u64, _vp]),
+    "gfp_vec_mul_crt_profile": (_int, [_u64p, _u64p, _i64, _u64p, _i64, _int, _u64,
+                                       ctypes.POINTER(ctypes.c_uint64),
+                                       ctypes.POINTER(ctypes.c_float), _vp]),
     "gfp_vec_pow": (_int, [_u64p, ctypes.POINTER(ctypes.c_uint64), _int, _u64p, _i64, _int,
                            _u64, _vp]),
     "gfp_vec_is_canonical": (_int, [_u64p, _vp, _i64, _int, _u64, _vp]),
@@ -62,6 +68,10 @@ SIGNATURES = {
     "gfp_poly_mul_host": (_int, [_vp, _u64p, _u64p, _u64p, _i64, _vp]),
     "gfp_poly_mul_host2": (_int, [_vp, _u64p, _i64, _u64p, _i64, _u64p, _i64, _vp]),
     "gfp_fft_plan_last_launches": (_i64, [_vp]),
+    "gfp_fft_plan_caps": (_int, [_vp]),
+    "gfp_fft_plan_set_timing": (_int, [_vp, _int]),
+    "gfp_fft_plan_pass_times": (_int, [_vp, ctypes.POINTER(ctypes.c_float),
+                                       ctypes.POINTER(ctypes.c_int), _int]),
     "gfp_fft_twiddle": (_int, [_vp, _u64p, _u64p, _i64, _i64, _i64, _int, _vp]),
     "gfp_exchange_transpose": (_int, [_u64p, ctypes.POINTER(ctypes.c_uint64), _int, _int, _i64,
                                       _int, _i64, _vp]),

@@ -3,6 +3,7 @@
 
     python -m paper_1811_01490_b200 bench-fft --K 16 --e 3 [--trials T] [--seed S] [--r R]
     python -m paper_1811_01490_b200 bench-mul --k 8,16,32 [--trials T]
+    python -m paper_1811_01490_b200 profile-mul --k 8,16,32 [--trials T]
     python -m paper_1811_01490_b200 verify --k 8 [--trials T] [--out cex.gfpv]
     python -m paper_1811_01490_b200 fft --in x.gfpv --out y.gfpv [--inverse]
     python -m paper_1811_01490_b200 polymul --in f.gfpv --in2 g.gfpv --out h.gfpv
@@ -211,10 +212,11 @@ def cmd_bench_fft(args, out=None):
         raise ValueError("backend %r is not available here (gfp-cuda only)" % args.backend)
     trials = args.trials or 1
     w = csv.writer(out, lineterminator="\n")
-    # the reference's columns, then this backend's own split of the time
+    # the reference's columns (phases per fft.pass_profile), then the
+    # device-resident transform time
     w.writerow(["K", "e", "backend", "total_seconds", "permutation_seconds",
                 "basecase_seconds", "twiddle_seconds", "avg_mult_seconds", "verified",
-                "upload_seconds", "download_seconds", "device_seconds"])
+                "device_seconds"])
     for K in Ks:
         for e in es:
             k = K // 2
@@ -240,11 +242,11 @@ def cmd_bench_fft(args, out=None):
             x = gp.vec.to_device(v0, k)
             y = gp.vec.empty(k, N)
             dev = _device_seconds(lambda: gp.fft_tensor(x, plan, out=y), max(3, trials))
-            w.writerow([K, e, "gfp-cuda", "%.6f" % total, "%.6f" % 0.0,
-                        "%.6f" % (prof.get("transform", 0.0) / trials), "%.6f" % 0.0,
-                        "%.9f" % (total / _mult_count(K, e)), verified,
-                        "%.6f" % (prof.get("upload", 0.0) / trials),
-                        "%.6f" % (prof.get("download", 0.0) / trials), "%.6f" % dev])
+            w.writerow([K, e, "gfp-cuda", "%.6f" % total,
+                        "%.6f" % (prof.get("permutation", 0.0) / trials),
+                        "%.6f" % (prof.get("basecase", 0.0) / trials),
+                        "%.6f" % (prof.get("twiddle", 0.0) / trials),
+                        "%.9f" % (total / _mult_count(K, e)), verified, "%.6f" % dev])
     return 0
 
 
@@ -283,6 +285,40 @@ def cmd_bench_mul(args, out=None):
         w.writerow([k, r, round(statistics.mean(times) * 1e9),
                     round(statistics.median(times) * 1e9), "%.3f" % (dev / batch * 1e9), batch,
                     "yes"])
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# profile-mul (bench_cli.cmd_profile_mul, bench_cli.py:470-494)
+
+def cmd_profile_mul(args, out=None):
+    """Per-step percentages of the reference's multiply mechanism
+    (convert_in, convolution, convert_out, crt, lhc, final), measured on the
+    device: `trials` random pairs multiplied by the instrumented mechanism
+    kernel in one launch (gfp_vec_mul_crt_profile: SM cycles per step),
+    after a check against Python integers.  Same CSV as the reference."""
+    out = sys.stdout if out is None else out
+    gp = _gp()
+    ks = args.k_list or [8, 16, 32, 64]
+    trials = args.trials or 50
+    rng = random.Random(args.seed)
+    steps = gp.vec.MUL_STEPS
+    w = csv.writer(out, lineterminator="\n")
+    w.writerow(["k", "r"] + ["%s_pct" % s for s in steps])
+    for k in ks:
+        r = _radix_for(args, k)
+        params = gp.GfpParams(r, k)
+        gp.gfp_mult._require_compat(params, gp.crt_default())
+        p = params.p
+        pairs = [(rng.randrange(p), rng.randrange(p)) for _ in range(trials)]
+        x = gp.vec.to_device([gp.gfp_encode(params, a) for a, _ in pairs], k)
+        y = gp.vec.to_device([gp.gfp_encode(params, b) for _, b in pairs], k)
+        z, cycles, _ = gp.vec.mul_crt_profile(x, y, params)
+        for (a, b), t in zip(pairs, gp.vec.to_tuples(z)):
+            if gp.gfp_decode(params, t) != a * b % p:
+                raise SystemExit("backend mismatch at k=%d a=%d b=%d" % (k, a, b))
+        total = sum(cycles.values()) or 1
+        w.writerow([k, r] + ["%.2f" % (100.0 * cycles[s] / total) for s in steps])
     return 0
 
 
@@ -491,6 +527,7 @@ def build_parser():
     p = sub.add_parser("bench-mul", help="time the general multiply")
     common(p, k_list=True)
     p.add_argument("--batch", type=int, default=None, help="batched-throughput size")
+    common(sub.add_parser("profile-mul", help="per-step multiplication profile"), k_list=True)
     p = sub.add_parser("bench-fft", help="time a K^e DFT")
     common(p)
     p.add_argument("--K", dest="K_list", type=_int_list, default=None)
@@ -512,12 +549,13 @@ def build_parser():
 def main(argv=None):
     args = build_parser().parse_args(argv)
     out, opened = sys.stdout, None
-    if args.command in ("bench-mul", "bench-fft") and args.out:
+    if args.command in ("bench-mul", "bench-fft", "profile-mul") and args.out:
         opened = open(args.out, "w", newline="")
         out = opened
     try:
         fn = {"verify": cmd_verify, "bench-mul": cmd_bench_mul, "bench-fft": cmd_bench_fft,
-              "fft": cmd_fft, "polymul": cmd_polymul}[args.command]
+              "profile-mul": cmd_profile_mul, "fft": cmd_fft,
+              "polymul": cmd_polymul}[args.command]
         return fn(args, out)
     except ValueError as exc:  # ConfigurationError and GfpvFormatError included
         kind = "configuration error" if type(exc).__name__ == "ConfigurationError" else "error"

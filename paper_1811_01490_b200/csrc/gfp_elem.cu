@@ -407,18 +407,19 @@ __global__ void k_transpose(const u64 *__restrict__ src, u64 *__restrict__ dst, 
     }
 }
 
-static int g_num_sms = 0;
+static int g_num_sms[64];  // per device id (0 = not queried yet)
 
 int num_sms()
 {
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0)
-            g_num_sms = 148;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int &n = g_num_sms[dev & 63];
+    if (!n) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        n = v > 0 ? v : 148;
     }
-    return g_num_sms;
+    return n;
 }
 
 dim3 grid_for(int64_t work, int threads)

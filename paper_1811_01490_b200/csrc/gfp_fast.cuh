@@ -12,7 +12,7 @@
 //
 // with MID from a limb-level Karatsuba product (3 IMAD.WIDE per digit pair).
 //
-// The host verifies (plan time, exact integers: gfp_kernels.cu fast_bounds)
+// The host verifies (plan time, exact integers: gfp_elem.cu fast_bounds)
 // that every sub-column stays below 2^63 in magnitude for the digit bounds
 // the transform guarantees, so the accumulation needs no carries.  The
 // quotient of each biased column c' = c + 2^63 r (non-negative, < 2^64 r) by
@@ -35,7 +35,7 @@
 #endif
 
 // limb split used by the fast multiply for each k (compile time; the host
-// bound check in gfp_kernels.cu:fast_bounds verifies it for the given r)
+// bound check in gfp_elem.cu:fast_bounds verifies it for the given r)
 template <int KD>
 struct FastSplit {
     static constexpr int S = KD <= 16 ? 29 : 28;

@@ -20,14 +20,31 @@ dim3 grid_for(int64_t work, int threads);
 int cuda_status();
 int check_kr(int k, u64 r);
 
+// Run f once per CUDA device (function attributes such as the dynamic
+// shared-memory limit apply per device context); `mask` holds one bit per
+// device id.  A benign race only repeats the idempotent f.
+template <typename F>
+inline void once_per_device(unsigned long long &mask, F &&f)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (__atomic_load_n(&mask, __ATOMIC_ACQUIRE) & bit)
+        return;
+    f();
+    __atomic_fetch_or(&mask, bit, __ATOMIC_ACQ_REL);
+}
+
 struct gfp_fft_plan;
+
+#define GFP_MAX_GRID_Y 65535  // pass kernels put the batch in grid.y
+#define GFP_MAX_TIMED 64  // pass launches timed per call (gfp_fft_plan_pass_times)
 
 struct PassArgs {
     const u64 *in;
     u64 *out;
     const u64 *table;  // element-major [M][k] balanced, omega^b (or omega^b / N)
     const u64 *table_lh;  // the same entries as limb pairs l | h << 32 (k_pass44)
-    const u64 *table_lh_plain;  // omega^b limb pairs even when scale (k_pass256's outer twiddle)
     const u64 *pre;    // optional pointwise operand, digit-major like `in`
     const u64 *in2;    // optional second set of `batch` vectors (grid.y >= batch)
     u64 *out2;
@@ -104,13 +121,15 @@ struct gfp_fft_plan {
     int64_t h_words;
     int64_t last_launches;
     int root_inv;  // omega^(N/2k) == 1/r (a plan built on an inverse root)
+    // per-launch timing of the last call (gfp_fft_plan_set_timing)
+    int timing, n_ev;
+    cudaEvent_t ev[GFP_MAX_TIMED + 1];
+    int ev_pass[GFP_MAX_TIMED];
 };
 
 // one radix-K Stockham pass (gfp_pass.cuh), instantiated per k in gfp_pass_k*.cu
 // true when the pass kernels of this plan take element-major I/O (PassIO)
 bool em_io_supported(const gfp_fft_plan *p);
-// true when pairs of passes run as one k_pass256 launch (k = 8, mode 3, N >= 1024)
-bool pass256_ok(const gfp_fft_plan *p);
 
 // em: element-major first-pass input / last-pass output (nullptr: none);
 // returns GFP_EUNSUPPORTED when em is requested but the kernel for this k
@@ -120,12 +139,6 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2, 
                 const u64 *pre, int64_t batch, int64_t Ns, int inverse, int scale, int canon,
                 int in_canon, const PassIO *em, cudaStream_t st);
 
-// two consecutive passes (Ns, K Ns) in one launch (k_pass256; k = 8 only):
-// GFP_EUNSUPPORTED when the pair kernel does not apply
-template <int KD>
-int launch_pass_pair(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2, u64 *out2,
-                     const u64 *pre, int64_t batch, int64_t Ns, int inverse, int scale,
-                     int canon, int in_canon, cudaStream_t st);
 
 #define DISPATCH_K(k, CALL)                                                                     \
     switch (k) {                                                                                \

@@ -104,12 +104,67 @@ __device__ __forceinline__ void ntt(u64 (&a)[KD], const u64 *pw, const WordC &c)
     }
 }
 
+// phase clock (profile instantiation only): SM cycle counter, ordered
+// against the surrounding code by the asm barrier
+__device__ __forceinline__ long long phase_clock()
+{
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+    return t;
+}
+
+// the crt step for coefficient i: the signed coefficient v in
+// [-(P1 P2 - 1)/2, (P1 P2 - 1)/2] as (|v|, sign) (crt_combine, gfp_mult.py:184-198)
+__device__ __forceinline__ u128 crt_coeff(u64 a1, u64 a2, const CrtConsts &C, bool &neg)
+{
+    const u64 r1 = cm_mul(a1, C.m2r1, C.w[0]);  // a1 m2 mod q1
+    const u64 r2 = cm_mul(a2, C.m1r2, C.w[1]);  // a2 m1 mod q2
+    u128 v = (u128)r1 * C.w[1].q + (u128)r2 * C.w[0].q;
+    if (v >= C.q1q2)
+        v -= C.q1q2;
+    neg = v > C.half;
+    if (neg)
+        v = C.q1q2 - v;
+    return v;
+}
+
+// the final step for one LHC triple: +-(l + h r + c r^2) r^i into the
+// signed digit accumulators (each wrap past r^k flips the sign, r^k = -1)
 template <int KD>
+__device__ __forceinline__ void final_accumulate(i64 (&D)[KD], int i, u64 l, u64 h, u64 cc,
+                                                 bool neg)
+{
+    const i64 s = neg ? -1 : 1;
+    const i64 terms[3] = {(i64)l * s, (i64)h * s, (i64)cc * s};
+#pragma unroll
+    for (int t = 0; t < 3; t++) {
+        int pos = i + t;
+        i64 v_t = terms[t];
+        if (pos >= KD) {
+            pos -= KD;
+            v_t = -v_t;
+        }
+        if (pos >= KD) {  // k = 1 only: r^2 = (r^1)^2 = +1
+            pos -= KD;
+            v_t = -v_t;
+        }
+        D[pos] += v_t;
+    }
+}
+
+// PROF: the profile instantiation (gfp_mul_fft(profile=), the reference's
+// per-step keys, gfp_mult.py:428-500).  It runs the crt, lhc and final steps
+// as three separate loops over the coefficients (the product is the same)
+// and adds each thread's SM cycles per step into prof[0..5] = convert_in,
+// convolution, convert_out, crt, lhc, final.
+template <int KD, bool PROF>
 __global__ void __launch_bounds__(128) k_mul_crt(const u64 *__restrict__ x, const u64 *__restrict__ y,
                                                  int64_t y_inc, u64 *__restrict__ z, int64_t n,
-                                                 const __grid_constant__ CrtConsts C, RadixConsts rc)
+                                                 const __grid_constant__ CrtConsts C, RadixConsts rc,
+                                                 unsigned long long *prof)
 {
     const int64_t yn = y_inc ? n : 1;
+    long long cyc[6] = {0, 0, 0, 0, 0, 0};
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t ey = y_inc ? e : 0;
@@ -118,6 +173,7 @@ __global__ void __launch_bounds__(128) k_mul_crt(const u64 *__restrict__ x, cons
         for (int p = 0; p < 2; p++) {
             const WordC &c = C.w[p];
             u64 a[KD], b[KD];
+            long long t0 = PROF ? phase_clock() : 0;
             // convert_in
 #pragma unroll
             for (int i = 0; i < KD; i++) {
@@ -127,6 +183,11 @@ __global__ void __launch_bounds__(128) k_mul_crt(const u64 *__restrict__ x, cons
                 a[i] = cm_mul(xv, C.in_t[p][i], c);
                 b[i] = cm_mul(yv, C.in_t[p][i], c);
             }
+            if (PROF) {
+                const long long t1 = phase_clock();
+                cyc[0] += t1 - t0;
+                t0 = t1;
+            }
             // convolution
             ntt<KD>(a, C.pw[p], c);
             ntt<KD>(b, C.pw[p], c);
@@ -134,45 +195,55 @@ __global__ void __launch_bounds__(128) k_mul_crt(const u64 *__restrict__ x, cons
             for (int i = 0; i < KD; i++)
                 a[i] = cm_mul(a[i], b[i], c);
             ntt<KD>(a, C.pwi[p], c);
+            if (PROF) {
+                const long long t1 = phase_clock();
+                cyc[1] += t1 - t0;
+                t0 = t1;
+            }
             // convert_out
 #pragma unroll
             for (int i = 0; i < KD; i++)
                 res[p][i] = cm_mul(a[i], C.out_t[p][i], c);
+            if (PROF)
+                cyc[2] += phase_clock() - t0;
         }
         // crt + lhc + final: signed digit accumulators D (r^k = -1 wraps)
         i64 D[KD];
 #pragma unroll
         for (int i = 0; i < KD; i++)
             D[i] = 0;
+        long long t0 = PROF ? phase_clock() : 0;
+        if constexpr (PROF) {
+            u128 v[KD];
+            bool neg[KD];
 #pragma unroll
-        for (int i = 0; i < KD; i++) {
-            const u64 r1 = cm_mul(res[0][i], C.m2r1, C.w[0]);  // a1 m2 mod q1
-            const u64 r2 = cm_mul(res[1][i], C.m1r2, C.w[1]);  // a2 m1 mod q2
-            u128 v = (u128)r1 * C.w[1].q + (u128)r2 * C.w[0].q;
-            if (v >= C.q1q2)
-                v -= C.q1q2;
-            const bool neg = v > C.half;
-            if (neg)
-                v = C.q1q2 - v;
-            // |v| < k r^2 (host-checked gate): v = l + h r + c r^2
-            u64 l, h, cc;
-            const u64 q1 = div128_by_r((u64)(v >> 64), (u64)v, rc, l);  // v / r < k r < 2^64
-            cc = div128_by_r(0, q1, rc, h);
-            const i64 s = neg ? -1 : 1;
-            const i64 terms[3] = {(i64)l * s, (i64)h * s, (i64)cc * s};
+            for (int i = 0; i < KD; i++)
+                v[i] = crt_coeff(res[0][i], res[1][i], C, neg[i]);
+            long long t1 = phase_clock();
+            cyc[3] += t1 - t0;
+            t0 = t1;
+            u64 L[KD], H[KD], Cc[KD];
 #pragma unroll
-            for (int t = 0; t < 3; t++) {  // r^(i + t), each wrap past r^k flips the sign
-                int pos = i + t;
-                i64 v_t = terms[t];
-                if (pos >= KD) {
-                    pos -= KD;
-                    v_t = -v_t;
-                }
-                if (pos >= KD) {  // k = 1 only: r^2 = (r^1)^2 = +1
-                    pos -= KD;
-                    v_t = -v_t;
-                }
-                D[pos] += v_t;
+            for (int i = 0; i < KD; i++) {
+                const u64 q1 = div128_by_r((u64)(v[i] >> 64), (u64)v[i], rc, L[i]);
+                Cc[i] = div128_by_r(0, q1, rc, H[i]);
+            }
+            t1 = phase_clock();
+            cyc[4] += t1 - t0;
+            t0 = t1;
+#pragma unroll
+            for (int i = 0; i < KD; i++)
+                final_accumulate<KD>(D, i, L[i], H[i], Cc[i], neg[i]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < KD; i++) {
+                bool neg;
+                const u128 v = crt_coeff(res[0][i], res[1][i], C, neg);
+                // |v| < k r^2 (host-checked gate): v = l + h r + c r^2
+                u64 l, h, cc;
+                const u64 q1 = div128_by_r((u64)(v >> 64), (u64)v, rc, l);  // v / r < k r < 2^64
+                cc = div128_by_r(0, q1, rc, h);
+                final_accumulate<KD>(D, i, l, h, cc, neg);
             }
         }
         // carries: digits into [0, r) with a final carry C (value = D - C,
@@ -198,6 +269,13 @@ __global__ void __launch_bounds__(128) k_mul_crt(const u64 *__restrict__ x, cons
 #pragma unroll
         for (int i = 0; i < KD; i++)
             z[(int64_t)i * n + e] = out[i];
+        if (PROF)
+            cyc[5] += phase_clock() - t0;
+    }
+    if (PROF) {
+#pragma unroll
+        for (int s = 0; s < 6; s++)
+            atomicAdd(prof + s, (unsigned long long)cyc[s]);
     }
 }
 
@@ -270,8 +348,8 @@ static void make_crt_consts(int k, CrtConsts &C)
 
 }  // namespace
 
-extern "C" int gfp_vec_mul_crt(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z,
-                               int64_t n, int k, uint64_t r, void *stream)
+static int mul_crt_run(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z,
+                       int64_t n, int k, uint64_t r, unsigned long long *prof, cudaStream_t st)
 {
     int e = check_kr(k, r);
     if (e)
@@ -285,16 +363,57 @@ extern "C" int gfp_vec_mul_crt(const uint64_t *x, const uint64_t *y, int64_t y_i
     CrtConsts C;
     make_crt_consts(k, C);
     const RadixConsts rc = make_consts(k, r);
-    cudaStream_t st = (cudaStream_t)stream;
     const dim3 grid = grid_for(n, 128);
+#define MUL_CRT(KK)                                                                           \
+    if (prof)                                                                                 \
+        k_mul_crt<KK, true><<<grid, 128, 0, st>>>(x, y, y_inc, z, n, C, rc, prof);            \
+    else                                                                                      \
+        k_mul_crt<KK, false><<<grid, 128, 0, st>>>(x, y, y_inc, z, n, C, rc, nullptr);
     switch (k) {
-    case 1: k_mul_crt<1><<<grid, 128, 0, st>>>(x, y, y_inc, z, n, C, rc); break;
-    case 2: k_mul_crt<2><<<grid, 128, 0, st>>>(x, y, y_inc, z, n, C, rc); break;
-    case 4: k_mul_crt<4><<<grid, 128, 0, st>>>(x, y, y_inc, z, n, C, rc); break;
-    case 8: k_mul_crt<8><<<grid, 128, 0, st>>>(x, y, y_inc, z, n, C, rc); break;
-    case 16: k_mul_crt<16><<<grid, 128, 0, st>>>(x, y, y_inc, z, n, C, rc); break;
-    case 32: k_mul_crt<32><<<grid, 128, 0, st>>>(x, y, y_inc, z, n, C, rc); break;
-    default: k_mul_crt<64><<<grid, 128, 0, st>>>(x, y, y_inc, z, n, C, rc); break;
+    case 1: MUL_CRT(1) break;
+    case 2: MUL_CRT(2) break;
+    case 4: MUL_CRT(4) break;
+    case 8: MUL_CRT(8) break;
+    case 16: MUL_CRT(16) break;
+    case 32: MUL_CRT(32) break;
+    default: MUL_CRT(64) break;
     }
+#undef MUL_CRT
     return cuda_status();
+}
+
+extern "C" int gfp_vec_mul_crt(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z,
+                               int64_t n, int k, uint64_t r, void *stream)
+{
+    return mul_crt_run(x, y, y_inc, z, n, k, r, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int gfp_vec_mul_crt_profile(const uint64_t *x, const uint64_t *y, int64_t y_inc,
+                                       uint64_t *z, int64_t n, int k, uint64_t r,
+                                       uint64_t *step_cycles, float *ms, void *stream)
+{
+    if (!step_cycles)
+        return GFP_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long *d = nullptr;
+    if (cudaMalloc(&d, 6 * sizeof(unsigned long long)) != cudaSuccess)
+        return GFP_ENOMEM;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaEventCreate(&ev[0]);
+    cudaEventCreate(&ev[1]);
+    cudaMemsetAsync(d, 0, 6 * sizeof(unsigned long long), st);
+    cudaEventRecord(ev[0], st);
+    int err = mul_crt_run(x, y, y_inc, z, n, k, r, d, st);
+    cudaEventRecord(ev[1], st);
+    if (!err && cudaMemcpyAsync(step_cycles, d, 6 * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        err = GFP_ECUDA;
+    if (!err && cudaStreamSynchronize(st) != cudaSuccess)
+        err = GFP_ECUDA;
+    if (!err && ms)
+        cudaEventElapsedTime(ms, ev[0], ev[1]);
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    cudaFree(d);
+    return err;
 }

@@ -124,17 +124,10 @@ static inline int launch_mul_wide(int k, const u64 *x, const u64 *y, int64_t y_i
 {
     if (k != 32 || rc.stages_per_norm <= 0)
         return 0;
-    static int disabled = -1;
-    if (disabled < 0) {
-        const char *e = getenv("GFP_MUL_WIDE");  // experiment hook: 0 = thread-serial kernel
-        disabled = (e && e[0] == '0') ? 1 : 0;
-    }
-    if (disabled)
-        return 0;
     const int nt = 128;
     const size_t smem = sizeof(int4) * 32 * nt;
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;  // per device
+    once_per_device(attr, [&] {
         cudaFuncSetAttribute(k_mul_wide<32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         cudaFuncSetAttribute(k_mul_wide<32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -143,8 +136,7 @@ static inline int launch_mul_wide(int k, const u64 *x, const u64 *y, int64_t y_i
                              (int)smem);
         cudaFuncSetAttribute(k_mul_wide<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        attr = true;
-    }
+    });
     int64_t blocks = (n + nt - 1) / nt;
     const int64_t cap = (int64_t)num_sms() * 3 * 8;
     if (blocks > cap)

@@ -10,7 +10,7 @@
 #pragma once
 #include "gfp_internal.cuh"
 #include "gfp_fast.cuh"
-#include "gfp_pass256.cuh"
+#include "gfp_pass44.cuh"
 
 // k values whose pass multiply keeps the twiddle limbs in shared memory
 // (fast_mul_window_store) instead of registers
@@ -374,18 +374,6 @@ static int pass_threads(int k, int64_t M, int *G_out)
     // to give every SM two CTAs
     int Gmax = (k >= 16 ? 128 : 256) / k;
     int Gmin = 32 / k > 0 ? 32 / k : 1;
-    static int g_env = -1;
-    if (g_env < 0) {
-        const char *e = getenv("GFP_PASS_G");  // experiment hook: groups per CTA
-        g_env = e ? atoi(e) : 0;
-    }
-    if (g_env > 0) {
-        int G = g_env * Gmin;
-        if (G > Gmax)
-            G = Gmax;
-        *G_out = G;
-        return G * k;
-    }
     int G = Gmax;
     while (G > Gmin && (M + G - 1) / G < 2 * (int64_t)num_sms())
         G >>= 1;
@@ -402,7 +390,7 @@ static size_t pass_smem(int G)
            (PASS_WINDOW(KD) ? (size_t)KD * G * KD * sizeof(int2) : 0);
 }
 
-// the pass-kernel arguments shared by k_pass, k_pass44 and k_pass256
+// the pass-kernel arguments shared by k_pass and k_pass44
 static inline int make_pass_args(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
                                  u64 *out2, const u64 *pre, int64_t batch, int64_t Ns,
                                  int inverse, int scale, int canon, int in_canon,
@@ -413,7 +401,6 @@ static inline int make_pass_args(const gfp_fft_plan *p, const u64 *in, u64 *out,
     A.out = out;
     A.table = scale ? p->table_ninv : p->table;
     A.table_lh = scale ? p->table_ninv_lh : p->table_lh;
-    A.table_lh_plain = p->table_lh;
     A.pre = pre;
     A.batch_stride = (int64_t)p->k * p->N;
     A.lN = ilog2_exact(p->N);
@@ -483,8 +470,8 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
     int G;
     int threads = pass_threads(KD, p->M, &G);
     size_t smem = pass_smem<KD>(G);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static unsigned long long attr_set = 0;  // per device
+    once_per_device(attr_set, [&] {
         for (int m = 0; m < 3; m++) {
             const void *fn = m == 0 ? (const void *)k_pass<KD, 0>
                              : m == 1 ? (const void *)k_pass<KD, 1> : (const void *)k_pass<KD, 2>;
@@ -495,8 +482,9 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
             cudaFuncSetAttribute((const void *)k_pass<KD, 3>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)pass_smem<KD>(256 / KD));
-        attr_set = true;
-    }
+    });
+    if ((in2 ? 2 : 1) * batch > GFP_MAX_GRID_Y)  // the batch is grid.y (callers chunk)
+        return GFP_EINVAL;
     PassArgs A;
     int err = make_pass_args(p, in, out, in2, out2, pre, batch, Ns, inverse, scale, canon, in_canon,
                              em, G, A);
@@ -521,27 +509,4 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
         launch_pdl(k_pass<KD, 0>, grid, threads, st, A, smem);
     }
     return cuda_status();
-}
-
-// Two consecutive passes (Ns, 16 Ns) in one k_pass256 launch (k = 8, mode 3,
-// N >= 1024, no element-major / four-step I/O, not both the pointwise
-// operand and N^-1): GFP_EUNSUPPORTED otherwise (the caller runs two passes)
-template <int KD>
-int launch_pass_pair(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2, u64 *out2,
-                     const u64 *pre, int64_t batch, int64_t Ns, int inverse, int scale,
-                     int canon, int in_canon, cudaStream_t st)
-{
-    if constexpr (KD != 8) {
-        return GFP_EUNSUPPORTED;
-    } else {
-        if (!pass256_enabled(KD, p->rc, p->N) || (pre && scale))
-            return GFP_EUNSUPPORTED;
-        PassArgs A;
-        int err = make_pass_args(p, in, out, in2, out2, pre, batch, Ns, inverse, scale, canon,
-                                 in_canon, nullptr, 1, A);
-        if (err)
-            return err;
-        launch_pass256(A, p->N, in2 ? 2 * batch : batch, st);
-        return cuda_status();
-    }
 }

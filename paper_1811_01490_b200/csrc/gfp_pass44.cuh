@@ -32,38 +32,21 @@
 #include "gfp_internal.cuh"
 #include "gfp_fast.cuh"
 
-#ifndef P44_MINB
-#define P44_MINB 5  // CTAs per SM the NW = 4 variant is register-bounded for (96 regs)
-#endif
-#ifndef P44_SPLIT2
-#define P44_SPLIT2 1  // NW > 4: stage 2's outputs split over all NW warps (else 4 warps)
-#endif
-#ifndef P44_L2PF
-#define P44_L2PF 0  // NW = 4: bulk L2 prefetch of the next element's rows (measured: C4 5.07 -> 5.31 ms, off)
-#endif
-#ifndef P44_XT
-#define P44_XT 8  // transforms per CTA in the fused-exchange pass: 8 -> 64 B store segments
-                  // (measured at 1 GPU: sharded C4 5.237 ms with 4, 5.218 ms with 8)
-#endif
-#ifndef P44_MINB16
-#define P44_MINB16 1  // CTAs per SM the NW = 16 variant is register-bounded for
-#endif
-#ifndef P44_XCH_MINB
-#define P44_XCH_MINB 4  // CTAs/SM bound of the XCH variant (5: 96 regs + 220 B spills, sharded C4 5.19 -> 5.43 ms)
-#endif
-#ifndef P44_FAST0
-#define P44_FAST0 0  // NW = 4 multiply-free first pass, all loads issued first (measured C4 5.036 -> 5.062 ms: off)
-#endif
-#ifndef P44_AUNROLL
-#define P44_AUNROLL 1  // phase-A elements interleaved per thread (experiment hook)
-#endif
-#define P44_STR_(x) #x
-#define P44_UNROLL_(n) _Pragma(P44_STR_(unroll n))
-#define P44_UNROLL(n) P44_UNROLL_(n)
-#ifndef P44_PF_MINNW
-#define P44_PF_MINNW 8  // smallest NW that stages the next element with cp.async (NW = 4
-                        // keeps 40 KB smem for 5 CTAs / SM: measured 1.5% faster on C4)
-#endif
+// register bounds (CTAs per SM) of the instantiations: NW = 4 at 5 CTAs/SM
+// (96 registers; C4), its fused-exchange variant at 4 (128 registers: 5
+// spilled and measured slower), NW = 8 at 2, NW = 16 at 1 (2 CTAs/SM at 64
+// registers spilled: C2 0.076 -> 0.100 ms)
+#define P44_MINB 5
+#define P44_XCH_MINB 4
+#define P44_MINB16 1
+// stage 2's outputs split over all NW warps when NW > 4
+#define P44_SPLIT2 1
+// transforms per CTA in the fused-exchange pass: 8 -> 64 B store segments
+// (measured at 1 GPU: sharded C4 5.237 ms with 4, 5.218 ms with 8)
+#define P44_XT 8
+// smallest NW that stages the next element with cp.async (NW = 4 keeps
+// 40 KB smem for 5 CTAs / SM: measured 1.5% faster on C4)
+#define P44_PF_MINNW 8
 
 namespace p44 {
 
@@ -262,56 +245,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
     };
     if (pf)
         prefetch(0);
-    // Without staging (NW = 4: the smem would cost a CTA per SM), one lane
-    // per warp asks the TMA unit to pull the NEXT element's k digit rows
-    // (32 groups x 8 B = 256 B each, contiguous) into L2 while this element
-    // is multiplied: its loads then wait for L2, not HBM (the load waits
-    // were ~20% of the pass's stall samples).  The row set is the same
-    // whatever the rotation r^a, so the prefetch needs no twiddle.
-    const bool l2pf = P44_L2PF && !PF && !em_in && gpc == 32 && j0 + 32 <= M && !xch;
-    auto l2_prefetch = [&](int i) {
-        if (lane == 0) {
-            const u64 *src = in + j0 + ((int64_t)(w + NW * i) << lM);
-#pragma unroll
-            for (int r_ = 0; r_ < KD; r_++)
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], 256;" ::"l"(
-                                 src + ((int64_t)r_ << lN))
-                             : "memory");
-        }
-    };
     i64 e[4][KD];
-    // First pass with nothing to multiply (no twiddle at Ns = 1, no pointwise
-    // operand, no N^-1, no four-step twiddle), NW = 4: an HBM-bound stream.
-    // Issue all 16/NW elements' digit loads before parking any, so each
-    // thread has 4 x k loads in flight instead of k.
-    const bool fast0 = P44_FAST0 && NW == 4 && !xch && lNs == 0 && !pre && !A.scale &&
-                       !A.ft_lh && !em_in;
-    if (fast0) {
-        constexpr int EPT = 16 / NW;
-        i64 xa[EPT][KD];
-        const unsigned rowN = 1u << lN;
-#pragma unroll
-        for (int i = 0; i < EPT; i++) {
-            const u64 *src = in + j + ((int64_t)(w + NW * i) << lM);
-#pragma unroll
-            for (int d = 0; d < KD; d++)
-                xa[i][d] = active ? (i64)__ldcs(src + (unsigned)d * rowN) : 0;
-        }
-#pragma unroll
-        for (int i = 0; i < EPT; i++) {
-            if (A.in_canon && active)
-                to_balanced<KD>(xa[i], rc.r);
-            i64 *slot = sm + ((w + NW * i) * 32 + lane) * SLOT;
-#pragma unroll
-            for (int d = 0; d < KD; d += 2)
-                *reinterpret_cast<longlong2 *>(slot + d) = make_longlong2(xa[i][d], xa[i][d + 1]);
-        }
-    }
-    P44_UNROLL(P44_AUNROLL)
-    for (int i = 0; i < (fast0 ? 0 : 16 / NW); i++) {
+    for (int i = 0; i < 16 / NW; i++) {
         const int t = w + NW * i;
-        if (l2pf && i + 1 < 16 / NW)
-            l2_prefetch(i + 1);
         i64 f[KD], x[KD];
         int64_t b = 0;
         unsigned negx = 0;
@@ -624,29 +560,15 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
 // k_pass44 serves k = 8 when 4 lazy radix-2 stages fit the digit bounds
 static inline bool pass44_enabled(int k, const RadixConsts &rc)
 {
-    static int disabled = -1;
-    if (disabled < 0) {
-        const char *e = getenv("GFP_PASS44");  // experiment hook: 0 = old kernel
-        disabled = (e && e[0] == '0') ? 1 : 0;
-    }
-    return k == 8 && !disabled && rc.stages_per_norm >= 4;
+    return k == 8 && rc.stages_per_norm >= 4;
 }
 
 // launch with programmatic stream serialisation (PDL): the kernel may start
 // while the previous kernel on the stream drains; it orders itself with
-// griddepcontrol.wait.  GFP_PDL=0 launches plainly.
+// griddepcontrol.wait
 static inline void launch_pdl(void (*kern)(PassArgs), dim3 grid, int threads, cudaStream_t st,
                               const PassArgs &A, size_t smem = 0)
 {
-    static int pdl = -1;
-    if (pdl < 0) {
-        const char *e = getenv("GFP_PDL");
-        pdl = (e && e[0] == '0') ? 0 : 1;
-    }
-    if (!pdl) {
-        kern<<<grid, threads, smem, st>>>(A);
-        return;
-    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(threads);
@@ -660,17 +582,17 @@ static inline void launch_pdl(void (*kern)(PassArgs), dim3 grid, int threads, cu
     cudaLaunchKernelEx(&cfg, kern, A);
 }
 
-// NW <= 8: dynamic shared memory for the cp.async staging rows ([NW][k][32])
+// NW <= 8: dynamic shared memory for the cp.async staging rows ([NW][k][32]);
+// the attribute is per device context, so it is set once per device
 template <int KD, int SP, bool IV, int NW, bool XCH = false>
 static inline void launch_p44(dim3 grid, cudaStream_t st, const PassArgs &A)
 {
     const size_t smem = NW >= P44_PF_MINNW ? (size_t)NW * KD * 32 * sizeof(u64) : 0;
-    static bool set = false;
-    if (!set) {
+    static unsigned long long set_on = 0;
+    once_per_device(set_on, [&] {
         cudaFuncSetAttribute(k_pass44<KD, SP, IV, NW, XCH>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        set = true;
-    }
+    });
     launch_pdl(k_pass44<KD, SP, IV, NW, XCH>, grid, NW * 32, st, A, smem);
 }
 
@@ -685,26 +607,11 @@ static int launch_pass44(const PassArgs &A0, int64_t M, int64_t nsets, cudaStrea
             return 0;
         const int64_t ctas = ((M + 31) / 32) * nsets;
         // elements per thread in phase A: 4 when the grid fills the GPU,
-        // fewer (more warps per CTA) for small transforms (C1, C2)
-        static int nw_env = -1;
-        if (nw_env < 0) {
-            const char *e = getenv("GFP_PASS44_NW");  // experiment hook
-            nw_env = e ? atoi(e) : 0;
-        }
-        int nw = ctas >= 4 * (int64_t)num_sms() ? 4 : ctas >= (int64_t)num_sms() ? 8 : 16;
-        if (nw_env == 4 || nw_env == 8 || nw_env == 16)
-            nw = nw_env;
-        // groups per CTA: 32.  (Spreading a grid under two waves over every
-        // SM with fewer groups per CTA was measured: no gain for C1 / C2,
-        // whose passes are latency-bound per CTA; kept as an experiment hook.)
+        // fewer (more warps per CTA) for small transforms (C1, C2).  Groups
+        // per CTA: 32 (spreading a grid under two waves over every SM with
+        // fewer was measured: no gain for C1 / C2, latency-bound per CTA).
+        const int nw = ctas >= 4 * (int64_t)num_sms() ? 4 : ctas >= (int64_t)num_sms() ? 8 : 16;
         int gpc = 32;
-        static int gpc_env = -1;
-        if (gpc_env < 0) {
-            const char *e = getenv("GFP_PASS44_GPC");  // experiment hook
-            gpc_env = e ? atoi(e) : 0;
-        }
-        if (gpc_env >= 1 && gpc_env <= 32)
-            gpc = gpc_env;
         PassArgs A = A0;
         if (A.xg)  // fused exchange: 8 groups x 4 transforms per CTA
             gpc = 32 / P44_XT;

@@ -5,5 +5,3 @@
 template int launch_pass<16>(const gfp_fft_plan *, const u64 *, u64 *, const u64 *, u64 *,
                              const u64 *, int64_t, int64_t, int, int, int, int, const PassIO *,
                              cudaStream_t);
-template int launch_pass_pair<16>(const gfp_fft_plan *, const u64 *, u64 *, const u64 *, u64 *,
-                                  const u64 *, int64_t, int64_t, int, int, int, int, cudaStream_t);

@@ -8,6 +8,3 @@ template int launch_pass<8>(const gfp_fft_plan *, const u64 *, u64 *, const u64 
 
 bool em_io_supported(const gfp_fft_plan *p) { return pass44_enabled(p->k, p->rc); }
 
-bool pass256_ok(const gfp_fft_plan *p) { return pass256_enabled(p->k, p->rc, p->N); }
-template int launch_pass_pair<8>(const gfp_fft_plan *, const u64 *, u64 *, const u64 *, u64 *,
-                                  const u64 *, int64_t, int64_t, int, int, int, int, cudaStream_t);

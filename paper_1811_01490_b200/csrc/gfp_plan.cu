@@ -167,6 +167,33 @@ __global__ void k_twiddle_rows(const u64 *__restrict__ x, u64 *__restrict__ out,
     }
 }
 
+// Per-launch device timing (gfp_fft_plan_set_timing): with timing on, an
+// event is recorded on the launching stream before the first pass launch of
+// a call and after every pass launch, so consecutive events bracket exactly
+// one pass kernel.  pass >= 0 labels the launch just completed.
+static void timing_mark(gfp_fft_plan *p, cudaStream_t st, int pass)
+{
+    if (!p->timing)
+        return;
+    if (pass < 0 && p->n_ev > 0)  // before a launch: only the call's first one needs a start
+        return;
+    if (p->n_ev >= GFP_MAX_TIMED + 1)
+        return;
+    if (!p->ev[p->n_ev] && cudaEventCreate(&p->ev[p->n_ev]) != cudaSuccess)
+        return;
+    cudaEventRecord(p->ev[p->n_ev], st);
+    if (pass >= 0 && p->n_ev > 0)
+        p->ev_pass[p->n_ev - 1] = pass;
+    p->n_ev++;
+}
+
+// start of an API call on the plan: launch count and timing marks reset
+static void begin_call(gfp_fft_plan *p)
+{
+    p->last_launches = 0;
+    p->n_ev = 0;
+}
+
 // One transform of `batch` vectors (and, when in_b is given, a second
 // independent set of `batch` vectors transformed in the same launches).
 // in_canon: the input is canonical (user data) and is converted to balanced
@@ -178,29 +205,13 @@ static int run_transform2(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, c
                           u64 *out_b, u64 *work_b, const u64 *pre, int64_t batch, int inverse,
                           int in_canon, int out_canon, cudaStream_t st, const PassIO *em = nullptr)
 {
-    // launch schedule: pairs of passes in one k_pass256 launch where it
-    // applies (not the element-major first / last pass of the host paths,
-    // not a four-step first pass), single passes otherwise
+    // one Stockham pass per launch; ping-pong so that the last launch lands
+    // in `out`; inputs are never written
     const int e = p->e;
-    int span[64], nl = 0;
-    {
-        int pass = 0;
-        while (pass < e) {
-            const bool em_first = em && pass == 0 && (em->in || em->ft);
-            const bool em_last =
-                em && pass + 1 == e - 1 && ((em->out && out_canon) || em->xg);
-            const bool pair = pass + 1 < e && !em_first && !em_last && p->k == 8 &&
-                              pass256_ok(p) && !(pass == 0 && pre && inverse && pass + 1 == e - 1);
-            span[nl++] = pair ? 2 : 1;
-            pass += pair ? 2 : 1;
-        }
-    }
-    // ping-pong so that the last launch lands in `out`; inputs are never written
     const u64 *src = in, *src_b = in_b;
     int64_t Ns = 1;
-    int pass = 0;
-    for (int l = 0; l < nl; l++) {
-        const int remaining = nl - l;  // launches left including this one
+    for (int pass = 0; pass < e; pass++) {
+        const int remaining = e - pass;  // launches left including this one
         u64 *dst = (remaining % 2 == 1) ? out : work;
         if (dst == src)
             dst = (dst == out) ? work : out;
@@ -210,28 +221,21 @@ static int run_transform2(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, c
             if (dst_b == src_b)
                 dst_b = (dst_b == out_b) ? work_b : out_b;
         }
-        const int last = pass + span[l] == e;
+        const int last = pass + 1 == e;
         const int scale = inverse && last;
         const u64 *pre_p = pass == 0 ? pre : nullptr;
         int rcode = GFP_EUNSUPPORTED;
-        if (span[l] == 2) {
-            DISPATCH_FAST_K(p->k, (rcode = launch_pass_pair<KD>(p, src, dst, src_b, dst_b, pre_p,
-                                                                batch, Ns, inverse, scale,
-                                                                last && out_canon,
-                                                                pass == 0 && in_canon, st)));
-        } else {
-            DISPATCH_FAST_K(p->k, (rcode = launch_pass<KD>(p, src, dst, src_b, dst_b, pre_p, batch,
-                                                           Ns, inverse, scale, last && out_canon,
-                                                           pass == 0 && in_canon, em, st)));
-        }
+        timing_mark(p, st, -1);
+        DISPATCH_FAST_K(p->k, (rcode = launch_pass<KD>(p, src, dst, src_b, dst_b, pre_p, batch, Ns,
+                                                       inverse, scale, last && out_canon,
+                                                       pass == 0 && in_canon, em, st)));
         if (rcode)
             return rcode;
+        timing_mark(p, st, pass);
         p->last_launches++;
         src = dst;
         src_b = dst_b;
-        for (int i = 0; i < span[l]; i++)
-            Ns *= p->K;
-        pass += span[l];
+        Ns *= p->K;
     }
     if (em && ((em->out && out_canon) || em->xg))
         return cuda_status();  // the last pass wrote the element-major output / the exchange
@@ -444,6 +448,9 @@ int gfp_fft_plan_destroy(gfp_fft_plan *p)
     cudaFree(p->table_lh);
     cudaFree(p->table_ninv_lh);
     cudaFree(p->h_dev);
+    for (int i = 0; i <= GFP_MAX_TIMED; i++)
+        if (p->ev[i])
+            cudaEventDestroy(p->ev[i]);
     free(p);
     return GFP_OK;
 }
@@ -457,15 +464,58 @@ int64_t gfp_fft_workspace_words(const gfp_fft_plan *p, int64_t batch)
 
 int64_t gfp_fft_plan_last_launches(const gfp_fft_plan *p) { return p ? p->last_launches : 0; }
 
+int gfp_fft_plan_caps(const gfp_fft_plan *p)
+{
+    if (!p || !em_io_supported(p))
+        return 0;
+    return GFP_CAP_EM_IO | (p->e >= 2 ? GFP_CAP_FT | GFP_CAP_XCH : 0);
+}
+
+int gfp_fft_plan_set_timing(gfp_fft_plan *p, int on)
+{
+    if (!p)
+        return GFP_EINVAL;
+    p->timing = on ? 1 : 0;
+    p->n_ev = 0;
+    return GFP_OK;
+}
+
+int gfp_fft_plan_pass_times(gfp_fft_plan *p, float *ms, int *pass, int max)
+{
+    if (!p || max < 0)
+        return -GFP_EINVAL;
+    const int n = p->n_ev > 0 ? p->n_ev - 1 : 0;
+    if (n == 0)
+        return 0;
+    if (cudaEventSynchronize(p->ev[n]) != cudaSuccess)
+        return -GFP_ECUDA;
+    int i = 0;
+    for (; i < n && i < max; i++) {
+        if (ms && cudaEventElapsedTime(&ms[i], p->ev[i], p->ev[i + 1]) != cudaSuccess)
+            return -GFP_ECUDA;
+        if (pass)
+            pass[i] = p->ev_pass[i];
+    }
+    return i;
+}
+
 int gfp_fft_exec(const gfp_fft_plan *cp, const uint64_t *in, uint64_t *out, uint64_t *work,
                  int64_t batch, int inverse, void *stream)
 {
     gfp_fft_plan *p = const_cast<gfp_fft_plan *>(cp);
     if (!p || !in || !out || !work || batch < 1)
         return GFP_EINVAL;
-    p->last_launches = 0;
-    return run_transform(p, in, out, work, nullptr, batch, inverse ? 1 : 0, 1, 1,
-                         (cudaStream_t)stream);
+    begin_call(p);
+    // the batch is the pass kernels' grid.y: chunks of at most 65535 vectors
+    const int64_t vw = (int64_t)p->k * p->N;
+    for (int64_t b0 = 0; b0 < batch; b0 += GFP_MAX_GRID_Y) {
+        const int64_t nb = batch - b0 < GFP_MAX_GRID_Y ? batch - b0 : GFP_MAX_GRID_Y;
+        const int err = run_transform(p, in + b0 * vw, out + b0 * vw, work, nullptr, nb,
+                                      inverse ? 1 : 0, 1, 1, (cudaStream_t)stream);
+        if (err)
+            return err;
+    }
+    return GFP_OK;
 }
 
 int gfp_fft_exec_ex(const gfp_fft_plan *cp, const uint64_t *in, uint64_t *out, uint64_t *work,
@@ -477,7 +527,7 @@ int gfp_fft_exec_ex(const gfp_fft_plan *cp, const uint64_t *in, uint64_t *out, u
         return GFP_EINVAL;
     if (ft && (in_canon || ft->k != p->k || !em_io_supported(p)))
         return ft->k != p->k || in_canon ? GFP_EINVAL : GFP_EUNSUPPORTED;
-    p->last_launches = 0;
+    begin_call(p);
     PassIO io = {nullptr, nullptr, 0, 0, nullptr, 0, ft, ft_row0, ft_inverse ? 1 : 0};
     return run_transform(p, in, out, work, nullptr, batch, inverse ? 1 : 0, in_canon ? 1 : 0,
                          out_canon ? 1 : 0, (cudaStream_t)stream, ft ? &io : nullptr);
@@ -497,7 +547,7 @@ int gfp_fft_exec_exchange(const gfp_fft_plan *cp, const uint64_t *in, uint64_t *
     if (p->k != 8 || p->e < 2 || world > 8 || (world & (world - 1)) || batch % 8 ||
         !em_io_supported(p))
         return GFP_EUNSUPPORTED;
-    p->last_launches = 0;
+    begin_call(p);
     PassIO io = {nullptr, nullptr, 0, 0, nullptr, 0, nullptr, 0, 0, dst, world, rank};
     return run_transform(p, in, scratch, work, nullptr, batch, inverse ? 1 : 0, in_canon ? 1 : 0,
                          out_canon ? 1 : 0, (cudaStream_t)stream, &io);
@@ -510,16 +560,25 @@ int gfp_poly_mul(const gfp_fft_plan *cp, const uint64_t *f, const uint64_t *g, u
     if (!p || !f || !g || !out || !work || batch < 1)
         return GFP_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
-    p->last_launches = 0;
-    int64_t vw = (int64_t)p->k * p->N * batch;
-    u64 *G = work;        // DFT(g)
-    u64 *scratch = work + vw;
-    u64 *scratch_b = work + 2 * vw;
-    // out = DFT(f) and G = DFT(g) in the same launches; the spectra stay
-    // balanced lazy digits, only the product is canonicalised
-    int err = run_transform2(p, f, out, scratch, g, G, scratch_b, nullptr, batch, 0, 1, 0, st);
-    if (!err)  // out = IDFT(out .* G), the pointwise product fused into pass 0
-        err = run_transform(p, out, out, scratch, G, batch, 1, 0, 1, st);
+    begin_call(p);
+    // both operands share grid.y: chunks of at most 32767 products
+    constexpr int64_t CH = GFP_MAX_GRID_Y / 2;
+    const int64_t ew = (int64_t)p->k * p->N;
+    int err = GFP_OK;
+    for (int64_t b0 = 0; b0 < batch && !err; b0 += CH) {
+        const int64_t nb = batch - b0 < CH ? batch - b0 : CH;
+        const int64_t vw = ew * nb;
+        u64 *G = work;  // DFT(g)
+        u64 *scratch = work + vw;
+        u64 *scratch_b = work + 2 * vw;
+        u64 *o = out + b0 * ew;
+        // o = DFT(f) and G = DFT(g) in the same launches; the spectra stay
+        // balanced lazy digits, only the product is canonicalised
+        err = run_transform2(p, f + b0 * ew, o, scratch, g + b0 * ew, G, scratch_b, nullptr, nb, 0,
+                             1, 0, st);
+        if (!err)  // o = IDFT(o .* G), the pointwise product fused into pass 0
+            err = run_transform(p, o, o, scratch, G, nb, 1, 0, 1, st);
+    }
     return err;
 }
 
@@ -542,12 +601,8 @@ static int ensure_host_scratch(gfp_fft_plan *p, int64_t words)
 // no transpose kernel).  Pageable memory returns nullptr: the caller stages.
 static u64 *mapped_alias(const void *h)
 {
-    static int zc = -1;
-    if (zc < 0) {
-        const char *e = getenv("GFP_ZERO_COPY");  // experiment hook: 0 = stage with DMA copies
-        zc = (e && e[0] == '0') ? 0 : 1;
-    }
-    if (!zc)
+    // the pass kernels access element-major host rows with 16 B vectors
+    if ((uintptr_t)h & 15)
         return nullptr;
     cudaPointerAttributes at;
     if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
@@ -601,7 +656,7 @@ int gfp_poly_mul_host2(gfp_fft_plan *p, const uint64_t *f, int64_t nf, const uin
     const int k = p->k;
     const int64_t N = p->N, vw = (int64_t)k * N * batch;
     const int64_t n_out = nf + ng - 1 < N ? nf + ng - 1 : N;
-    p->last_launches = 0;
+    begin_call(p);
     if (!em_io_supported(p)) {
         int err = poly_mul_host_staged(p, f, nf, g, ng, out, n_out, batch, st);
         if (err)
@@ -666,7 +721,7 @@ int gfp_fft_exec_host(gfp_fft_plan *p, uint64_t *v, int64_t batch, int inverse, 
     cudaStream_t st = (cudaStream_t)stream;
     const int k = p->k;
     const int64_t N = p->N, vw = (int64_t)k * N * batch;
-    p->last_launches = 0;
+    begin_call(p);
     u64 *mv = em_io_supported(p) ? mapped_alias(v) : nullptr;
     // a single-pass transform would read and write v in the same launch:
     // stage its output

@@ -307,6 +307,8 @@ static int word_run(const gfp_word_plan *p, const u64 *in, u64 *out, int64_t bat
                     const u64 *w_in, const u64 *pre, const u64 *w_out, u64 scale, u64 *work,
                     cudaStream_t st)
 {
+    if (batch > GFP_MAX_GRID_Y)  // the batch is the pass kernels' grid.y
+        return GFP_EINVAL;
     const int lN = p->lN;
     int radices[64], np = 0, rem = lN;
     while (rem >= 4) {

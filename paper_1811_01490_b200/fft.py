@@ -11,8 +11,8 @@ plus the tensor-level API the data-parallel path is built for:
 
 The schedule is not the reference's (right-to-left stride permutations,
 separate twiddle stages): each of the e passes is one Stockham radix-K
-kernel (csrc/gfp_kernels.cu: k_pass) that reads K elements at stride N/K,
-multiplies by omega^E (the r^a part of omega^E = r^a omega^b folded into a
+kernel (csrc/gfp_pass44.cuh k_pass44 for k = 8, csrc/gfp_pass.cuh k_pass
+otherwise) that reads K elements at stride N/K, multiplies by omega^E (the r^a part of omega^E = r^a omega^b folded into a
 digit rotation, the reference's cheap-twiddle split, fft.py:84-103),
 runs the K-point DFT at root r with shift-only butterflies, and writes in
 natural order.  The output is the unique canonical encoding of the DFT, so it
@@ -121,16 +121,26 @@ def build_plan(field, K, e, omega, cheap_twiddle=None, threads=1):
     primitive N-th root, K != 2k, or omega^(N/2k) is neither r nor 1/r --
     the reference's rejections, checked on the device.
     """
-    from .word import MontField, build_word_plan
-    if isinstance(field, MontField):  # the word-prime transform (csrc/gfp_word.cu)
+    from .word import build_word_plan
+    # The reference accepts any object of its field protocol (fft.py:13-17).
+    # The device transform is chosen by the field's structure, not its class,
+    # so the reference's own field objects plug in too:
+    #   word-prime fields (a Montgomery context .ctx with .q, like MontField,
+    #   fft.py:376-421) -> the word-prime transform (csrc/gfp_word.cu);
+    #   shift-capable GFP fields (.params with r, k, plus shift_root / two_k,
+    #   like GfpFftField, gfp_mult.py:518-592) -> the GFP transform.
+    ctx = getattr(field, "ctx", None)
+    if ctx is not None and hasattr(ctx, "q") and hasattr(ctx, "one_mont"):
         return build_word_plan(field, K, e, omega)
     if K not in BASE_SIZES:
         raise ValueError("unsupported base-case size")
     if e < 1:
         raise ValueError("e must be at least 1")
     params = getattr(field, "params", None)
-    if params is None or not hasattr(field, "shift_root"):
-        raise ValueError("the GPU transform needs a GfpFftField (shift-capable GFP field)")
+    if (params is None or not hasattr(params, "r") or not hasattr(params, "k")
+            or not hasattr(field, "shift_root") or not hasattr(field, "two_k")):
+        raise ValueError("no device transform for this field: the GPU path covers GF(r^k + 1) "
+                         "fields (GfpFftField protocol) and word-prime Montgomery fields")
     if K != field.two_k:
         raise ValueError("base-case size must equal 2k for this field")
     k = params.k
@@ -256,9 +266,8 @@ def poly_mul_host(f, g, plan):
 def dft_general(v, plan, field=None, profile=None):
     """In-place DFT of K^e points (fft.py:298-360); returns v.
 
-    profile, when given, accumulates wall seconds under "upload",
-    "transform" and "download" (the device fuses the reference's
-    permutation / basecase / twiddle phases into one kernel per pass).
+    profile, when given, accumulates seconds under the reference's phase
+    keys "permutation", "basecase" and "twiddle" (see pass_profile).
     """
     from .word import WordPlan, dft_word
     if isinstance(plan, WordPlan):
@@ -280,21 +289,53 @@ def dft_inverse(v, plan, field=None, profile=None):
     return v
 
 
-def _tick(profile, key, t0):
-    if profile is not None:
-        torch.cuda.synchronize()
-        profile[key] = profile.get(key, 0.0) + (time.perf_counter() - t0)
-    return time.perf_counter()
+def pass_times(plan, fn):
+    """Run fn() with per-pass device timing on plan; returns fn's result and
+    [(pass index, ms)] of its pass launches (gfp_fft_plan_pass_times)."""
+    lib = _lib.load()
+    _lib.check(lib.gfp_fft_plan_set_timing(plan.handle, 1), "gfp_fft_plan_set_timing")
+    try:
+        res = fn()
+        ms = (ctypes.c_float * 64)()
+        idx = (ctypes.c_int * 64)()
+        n = lib.gfp_fft_plan_pass_times(plan.handle, ms, idx, 64)
+        if n < 0:
+            _lib.check(-n, "gfp_fft_plan_pass_times")
+    finally:
+        lib.gfp_fft_plan_set_timing(plan.handle, 0)
+    return res, [(int(idx[i]), float(ms[i])) for i in range(n)]
+
+
+def pass_profile(passes, moved_seconds):
+    """The reference's dft_general phases (fft.py:298-360) from the device
+    passes.  The GPU fuses the phases: each Stockham pass applies one level's
+    twiddles (none in the first pass) and one layer of K-point base cases,
+    and the stride permutations are its load / store indexing.  So:
+      basecase    = the first pass (base cases only, no twiddle);
+      twiddle     = the later passes (each a level's twiddle multiplies --
+                    the bulk of its instructions -- fused with its layer of
+                    base cases; the inverse's N^-1 scale rides on the last);
+      permutation = the data movement outside the passes (host list ->
+                    device digit-major vectors and back)."""
+    base = sum(ms for i, ms in passes if i == 0) * 1e-3
+    tw = sum(ms for i, ms in passes if i > 0) * 1e-3
+    return {"permutation": moved_seconds, "basecase": base, "twiddle": tw}
 
 
 def _run_list(v, plan, inverse, profile):
+    if profile is None:
+        v[:] = vec.to_tuples(fft(vec.to_device(v, plan.params.k), plan, inverse=inverse))
+        return
     t0 = time.perf_counter()
     x = vec.to_device(v, plan.params.k)
-    t0 = _tick(profile, "upload", t0)
-    y = fft(x, plan, inverse=inverse)
-    t0 = _tick(profile, "transform", t0)
+    torch.cuda.synchronize()
+    moved = time.perf_counter() - t0
+    y, passes = pass_times(plan, lambda: fft(x, plan, inverse=inverse))
+    t0 = time.perf_counter()
     v[:] = vec.to_tuples(y)
-    _tick(profile, "download", t0)
+    moved += time.perf_counter() - t0
+    for key, sec in pass_profile(passes, moved).items():
+        profile[key] = profile.get(key, 0.0) + sec
 
 
 _base_plans = {}

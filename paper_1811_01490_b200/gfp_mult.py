@@ -16,7 +16,6 @@ configuration contract is kept (CrtParams / crt_default hold the prime pair
 for check_prime_compat).
 """
 
-import time
 from dataclasses import dataclass
 from functools import lru_cache
 from typing import NamedTuple
@@ -97,24 +96,42 @@ def _require_compat(params, crt):
     _compat_ok[key] = True
 
 
+def add_step_profile(profile, cycles, seconds):
+    """Accumulate `seconds` of device time into profile under the reference's
+    step keys (gfp_mult.py:428-500), split by the measured per-step cycle
+    shares of the instrumented mechanism kernel."""
+    total = sum(cycles.values())
+    for step in vec.MUL_STEPS:
+        share = cycles[step] / total if total else 1.0 / len(vec.MUL_STEPS)
+        profile[step] = profile.get(step, 0.0) + seconds * share
+
+
 def _mul_device(params, x, y, profile=None, mechanism=False):
     if len(x) != params.k or len(y) != params.k:
         raise ValueError("element must have k digits")
-    t0 = time.perf_counter() if profile is not None else 0
     a = vec.to_device([x], params.k)
     b = vec.to_device([y], params.k)
     # mechanism: the reference's two-prime convolution + CRT + LHC route
     # (gfp_vec_mul_crt); else the direct exact multiply the transforms use
-    z = vec.mul_crt(a, b, params) if mechanism and params.k <= 64 else vec.mul(a, b, params)
-    out = vec.to_tuples(z)[0]
-    if profile is not None:
-        profile["device_mul"] = profile.get("device_mul", 0.0) + time.perf_counter() - t0
-    return out
+    if mechanism and params.k <= 64:
+        if profile is not None:
+            # the instrumented mechanism kernel: per-step cycles, device time
+            z, cycles, ms = vec.mul_crt_profile(a, b, params)
+            add_step_profile(profile, cycles, ms * 1e-3)
+        else:
+            z = vec.mul_crt(a, b, params)
+    else:
+        z = vec.mul(a, b, params)
+    return vec.to_tuples(z)[0]
 
 
 def gfp_mul_fft(params, crt, x, y, profile=None):
-    """x * y mod p; raises ConfigurationError like the reference when the
-    prime pair cannot carry k r^2 (gfp_mult.py:416-422)."""
+    """x * y mod p through the reference's mechanism on the device; raises
+    ConfigurationError like the reference when the prime pair cannot carry
+    k r^2 (gfp_mult.py:416-422).  profile, when given, accumulates seconds
+    under the reference's keys convert_in, convolution, convert_out, crt,
+    lhc, final: the device time of the instrumented kernel split by its
+    per-step cycle counts."""
     _require_compat(params, crt)
     return _mul_device(params, x, y, profile, mechanism=True)
 

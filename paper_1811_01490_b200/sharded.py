@@ -307,11 +307,15 @@ class GpuShardOps:
         self.plans = {"N1": F.build_plan(field, K, e(N1), w1),
                       "N2": F.build_plan(field, K, e(N2), w2)}
         self.params = params
-        # the k_pass44 kernels fold the inter-stage twiddle into the next
-        # transform's first pass (gfp_fft_exec_ex); other k use the
-        # separate twiddle kernel
-        self.fused = params.k == 8 and min(e(N1), e(N2)) >= 2  # (single-pass plans
-        # would carry N^-1 and the twiddle in one pass: unfused)
+        # pass kernels that can fold the inter-stage twiddle into the next
+        # transform's first pass (gfp_fft_exec_ex; k_pass44: k = 8 and a
+        # radix with 4 lazy stages per normalisation) are used fused; the
+        # library reports it per plan.  Others take the separate twiddle
+        # kernel (and the standalone exchange kernel).
+        from . import _lib
+        lib = _lib.load()
+        self.fused = all(lib.gfp_fft_plan_caps(p.handle) & _lib.GFP_CAP_FT
+                         for p in self.plans.values())
 
     def fft(self, x, which, inverse):
         from .fft import fft

@@ -108,6 +108,26 @@ def mul_crt(x, y, params):
     return z
 
 
+MUL_STEPS = ("convert_in", "convolution", "convert_out", "crt", "lhc", "final")
+
+
+def mul_crt_profile(x, y, params):
+    """mul_crt through the instrumented kernel: (product, {step: SM cycles},
+    device ms) with the reference's step keys (gfp_mult.py:428-500)."""
+    _require_cuda(x, y)
+    z = torch.empty_like(x)
+    k, n = x.shape
+    y_inc = 0 if y.shape[1] == 1 and n != 1 else 1
+    if y_inc and y.shape != x.shape:
+        raise ValueError("shape mismatch")
+    cyc = (ctypes.c_uint64 * 6)()
+    ms = ctypes.c_float(0.0)
+    _lib.check(_lib.load().gfp_vec_mul_crt_profile(_ptr(x), _ptr(y), y_inc, _ptr(z), n, k,
+                                                  params.r, cyc, ctypes.byref(ms), _stream()),
+               "gfp_vec_mul_crt_profile")
+    return z, dict(zip(MUL_STEPS, (int(c) for c in cyc))), float(ms.value)
+
+
 def pow(x, e, params):
     """x^e for a non-negative Python int exponent shared by all elements."""
     _require_cuda(x)
