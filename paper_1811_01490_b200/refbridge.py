@@ -36,7 +36,7 @@ BACKEND = "gfp-cuda"
 def install(bench_cli):
     """Register the gfp-cuda backend in the given gfpfft.bench_cli module
     (idempotent); returns the module."""
-    if getattr(bench_cli, "_gfp_cuda_installed", False):
+    if BACKEND in bench_cli.BACKENDS and getattr(bench_cli._fft_bench_setup, "_gfp_cuda", False):
         return bench_cli
     ref_setup = bench_cli._fft_bench_setup
     ref_dft = bench_cli.dft_general
@@ -70,8 +70,9 @@ def install(bench_cli):
             return F.dft_general(v, plan, field, profile=profile)
         return ref_dft(v, plan, field, profile=profile)
 
-    bench_cli.BACKENDS = tuple(bench_cli.BACKENDS) + (BACKEND,)
+    setup._gfp_cuda = True
+    if BACKEND not in bench_cli.BACKENDS:
+        bench_cli.BACKENDS = tuple(bench_cli.BACKENDS) + (BACKEND,)
     bench_cli._fft_bench_setup = setup
     bench_cli.dft_general = dft_general
-    bench_cli._gfp_cuda_installed = True
     return bench_cli
