@@ -15,7 +15,15 @@
 // wrapped digits negated, because r^k = -1, so shifts
 // never need normalisation.
 #pragma once
+
+// balanced -> canonical digits by carry-lookahead (else a serial chain;
+// measured: C4 last pass 1.195 -> 1.070 ms, C2 graph 0.0758 -> 0.0738 ms)
+#ifndef GFP_CANON_CLA
+#define GFP_CANON_CLA 1
+#endif
 #include <stdint.h>
+
+#include <type_traits>
 
 typedef uint64_t u64;
 typedef int64_t i64;
@@ -373,9 +381,54 @@ GFP_D void lazy_to_canonical(const DF &f, DZ &z, int k, const RadixConsts &rc)
 // The same canonicalisation for a compile-time k, branch-free (selects
 // instead of the data-dependent loops above): the transform's last pass runs
 // it for every output, and the branchy form is ~1000 SASS instructions per
-// inlined copy.  Input: lazy digits with |f_i| < r - 1 (balanced or lazy).
+// inlined copy.  Input: lazy digits with |f_i| < r - 1 (balanced or lazy;
+// the carry-lookahead form needs only |f_i| < r).
 template <int KD>
 GFP_D void lazy_to_canonical_bf(const i64 (&f)[KD], u64 (&z)[KD], const RadixConsts &rc)
+#if GFP_CANON_CLA
+{
+    // Balanced digits (|f_i| < r, what the pass kernels hold after their
+    // normalisation) need at most one borrow per digit: z_i = f_i - b_i,
+    // + r when that is negative, with the borrow into digit i + 1
+    //   b_(i+1) = [f_i - b_i < 0] = g_i | (p_i & b_i),  g_i = [f_i < 0], p_i = [f_i = 0].
+    // The borrows are a carry-lookahead over two k-bit masks: the carries of
+    // the integer sum (g | p) + g (whose generate / propagate bits are g / p)
+    // -- no serial dependence between the digits.
+    static_assert(KD <= 32, "k + 1 borrow bits must fit the mask");
+    using Mask = typename std::conditional<(KD < 32), unsigned, unsigned long long>::type;
+    Mask g = 0, p = 0;
+#pragma unroll
+    for (int i = 0; i < KD; i++) {
+        g |= (Mask)(f[i] < 0) << i;
+        p |= (Mask)(f[i] == 0) << i;
+    }
+    const Mask gp = g | p;
+    const Mask b = (gp + g) ^ gp ^ g;  // bit i: borrow into digit i (bit k: out of the top)
+#pragma unroll
+    for (int i = 0; i < KD; i++) {
+        const i64 t = f[i] - (i64)((b >> i) & 1u);
+        z[i] = (u64)(((b >> (i + 1)) & 1u) ? t + (i64)rc.r : t);
+    }
+    // a borrow out of the top digit: value = Z + 1 (r^k = -1), carried
+    // through r - 1 digits; carrying out of the top means p - 1 (form B)
+    if ((b >> KD) & 1u) {
+        bool ca = true;
+#pragma unroll
+        for (int i = 0; i < KD; i++) {
+            const u64 v = z[i];
+            const bool zt = v == rc.r - 1;
+            z[i] = ca ? (zt ? 0 : v + 1) : v;
+            ca = ca && zt;
+        }
+        if (ca) {
+#pragma unroll
+            for (int i = 0; i < KD - 1; i++)
+                z[i] = 0;
+            z[KD - 1] = rc.r;
+        }
+    }
+}
+#else
 {
     const i64 r = (i64)rc.r;
     int C = 0;
@@ -409,3 +462,4 @@ GFP_D void lazy_to_canonical_bf(const i64 (&f)[KD], u64 (&z)[KD], const RadixCon
         }
     }
 }
+#endif

@@ -37,6 +37,9 @@
 #ifndef PASS16_MINB
 #define PASS16_MINB 3  // CTAs per SM the k = 16 pass is register-bounded for
 #endif
+#ifndef PASS_NOMUL_MINB
+#define PASS_NOMUL_MINB 5  // the multiply-free first pass (NOMUL) for k >= 16
+#endif
 
 template <int KD>
 GFP_D i64 rot_lane(i64 val, int t, int d, bool inverse)
@@ -114,9 +117,15 @@ __host__ __device__ constexpr int bitrev_c(int x)
 // omega^E, E = t (j mod Ns) (M / Ns), and writes the K-point DFT to
 // (j / Ns) Ns K + (j mod Ns) + u Ns.  After log_K N passes the output is the
 // natural-order DFT (the reference's dft_general result, fft.py:298-360).
-template <int KD, int SPARSE>
+//
+// NOMUL: the instantiation for a pass with nothing to multiply (the first
+// pass: no twiddle at Ns = 1, no pointwise operand, no N^-1) -- a pure
+// HBM stream without the multiply's registers, so more CTAs per SM.
+template <int KD, int SPARSE, bool NOMUL = false>
 __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
-                                  KD == 16 ? PASS16_MINB : KD == 32 ? PASS32_MINB : 1)
+                                  NOMUL && KD == 16 ? PASS_NOMUL_MINB
+                                  : NOMUL && KD == 32 ? 3  /* 68 KB smem: 3 CTAs / SM */
+                                  : KD == 16 ? PASS16_MINB : KD == 32 ? PASS32_MINB : 1)
     k_pass(PassArgs A)
 {
     constexpr int K = 2 * KD;
@@ -182,7 +191,7 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
                 x[d] = (i64)__ldg(src + (size_t)((unsigned)((d - as) & (KD - 1)) * rowN));
             if (A.in_canon)  // pass 0 only, where a = 0
                 to_balanced<KD>(x, rc.r);
-            if (pre) {  // pass 0 only (a = b = 0)
+            if (!NOMUL && pre) {  // pass 0 only (a = b = 0)
                 if constexpr (KD >= PRE_WINDOW_MINK && PASS_WINDOW(KD)) {
                     // through the window (registers: x only), product parked in
                     // the element's row and read back
@@ -217,7 +226,7 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
         }
         i64 *row = sm + (((int64_t)t << lG) + g) * ROW;
         // warp-uniform multiply: lanes with b = 0 multiply by table[0] = 1
-        if (__any_sync(FULL_MASK, active && (b || A.scale))) {
+        if (!NOMUL && __any_sync(FULL_MASK, active && (b || A.scale))) {
             if (active) {
                 const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(A.table_lh + b * KD);
                 if (PASS_WINDOW(KD)) {
@@ -355,7 +364,7 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
 #pragma unroll
             for (int d = 0; d < KD; d++)
                 f[d] = row[d];
-            lazy_to_canonical(f, c, KD, rc);
+            lazy_to_canonical_bf<KD>(f, c, rc);  // balanced digits (phase B)
 #pragma unroll
             for (int d = 0; d < KD; d++)
                 out[((int64_t)d << lN) + pos] = c[d];
@@ -382,12 +391,12 @@ static int pass_threads(int k, int64_t M, int *G_out)
 }
 
 template <int KD>
-static size_t pass_smem(int G)
+static size_t pass_smem(int G, bool nomul = false)
 {
     // [K][G][k + 1] element rows, plus the window multiply's y-limb columns
     // (k int2 per thread, G k threads) when it is on for this k
     return (size_t)(2 * KD) * G * (KD + 1) * sizeof(i64) +
-           (PASS_WINDOW(KD) ? (size_t)KD * G * KD * sizeof(int2) : 0);
+           (PASS_WINDOW(KD) && !nomul ? (size_t)KD * G * KD * sizeof(int2) : 0);
 }
 
 // the pass-kernel arguments shared by k_pass and k_pass44
@@ -478,10 +487,14 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)pass_smem<KD>(256 / KD));
         }
-        if constexpr (P2Radix<KD>::a != 0)
+        if constexpr (P2Radix<KD>::a != 0) {
             cudaFuncSetAttribute((const void *)k_pass<KD, 3>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)pass_smem<KD>(256 / KD));
+            cudaFuncSetAttribute((const void *)k_pass<KD, 3, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)pass_smem<KD>(256 / KD, true));
+        }
     });
     if ((in2 ? 2 : 1) * batch > GFP_MAX_GRID_Y)  // the batch is grid.y (callers chunk)
         return GFP_EINVAL;
@@ -497,7 +510,10 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
     dim3 grid((unsigned)((p->M + G - 1) / G), (unsigned)(in2 ? 2 * batch : batch));
     if constexpr (P2Radix<KD>::a != 0) {
         if (p->rc.p3_ok) {
-            launch_pdl(k_pass<KD, 3>, grid, threads, st, A, smem);
+            if (Ns == 1 && !pre && !scale)  // nothing to multiply in this pass
+                launch_pdl(k_pass<KD, 3, true>, grid, threads, st, A, pass_smem<KD>(G, true));
+            else
+                launch_pdl(k_pass<KD, 3>, grid, threads, st, A, smem);
             return cuda_status();
         }
     }

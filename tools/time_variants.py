@@ -29,14 +29,34 @@ plan2 = gp.build_plan(f8, 16, 4, gp.roots_for(p8, 1 << 16))
 f = gp.vec.uniform(1 << 16, p8, seed=1); g = gp.vec.uniform(1 << 16, p8, seed=2)
 out = torch.empty_like(f)
 res["c2_polymul_ms"] = timeit(lambda: gp.poly_mul(f, g, plan2, out=out), 100)
+import hashlib
+dig = lambda t: hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest()[:12]
+res["c2_digest"] = dig(out)
+# C2 as bench.py times it: the 8 pass launches replayed from a CUDA graph
+graph = torch.cuda.CUDAGraph(); s = torch.cuda.Stream(); s.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(s):
+    gp.poly_mul(f, g, plan2, out=out)
+    with torch.cuda.graph(graph, stream=s):
+        gp.poly_mul(f, g, plan2, out=out)
+torch.cuda.current_stream().wait_stream(s); torch.cuda.synchronize()
+res["c2_graph_ms"] = timeit(graph.replay, 100)
+plan1 = gp.build_plan(f8, 16, 3, gp.roots_for(p8, 4096))
+x1 = gp.vec.uniform(4096, p8, seed=9); y1 = torch.empty_like(x1)
+def c1():
+    gp.fft_tensor(x1, plan1, out=y1); gp.fft_tensor(y1, plan1, inverse=True, out=y1)
+res["c1_ms"] = timeit(c1, 100)
 plan4 = gp.build_plan(f8, 16, 6, gp.roots_for(p8, 1 << 24))
 x = gp.vec.uniform(1 << 24, p8, seed=4); y = torch.empty_like(x)
 res["c4_fwd_ms"] = timeit(lambda: gp.fft_tensor(x, plan4, out=y), 10)
+res["c4_digest"] = dig(y)
+from paper_1811_01490_b200 import fft as F
+res["c4_pass_ms"] = [round(ms, 4) for _, ms in F.pass_times(plan4, lambda: gp.fft_tensor(x, plan4, out=y))[1]]
 del x, y
 p16 = gp.GfpParams(R[16], 16); f16 = gp.GfpFftField(p16, backend="cuda")
 plan3 = gp.build_plan(f16, 32, 4, gp.roots_for(p16, 1 << 20))
 x = gp.vec.uniform(1 << 20, p16, seed=3, batch=8); y = torch.empty_like(x)
 res["c3x8_fwd_ms"] = timeit(lambda: gp.fft_tensor(x, plan3, out=y), 10)
+res["c3_digest"] = dig(y)
 del x, y
 p32 = gp.GfpParams(R[32], 32); f32 = gp.GfpFftField(p32, backend="cuda")
 a = gp.vec.uniform(1 << 22, p32, seed=51); b = gp.vec.uniform(1 << 22, p32, seed=52)
@@ -45,6 +65,7 @@ del a, b
 plan5 = gp.build_plan(f32, 64, 3, gp.roots_for(p32, 1 << 18))
 x = gp.vec.uniform(1 << 18, p32, seed=5); y = torch.empty_like(x)
 res["c5_fwd_ms"] = timeit(lambda: gp.fft_tensor(x, plan5, out=y), 10)
+res["c5_digest"] = dig(y)
 print(json.dumps(res))
 ''' % ROOT
 
