@@ -80,6 +80,14 @@ int gfp_vec_mul_pow_r(const uint64_t *x, uint64_t *z, int64_t n, int k, uint64_t
 int gfp_vec_mul(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z, int64_t n,
                 int k, uint64_t r, void *stream);
 
+/* Host-buffer element-wise product: x, y, z are element-major host arrays
+   uint64[n][k] (the reference's tuple order); H2D, layout conversion,
+   gfp_vec_mul, back; synchronous.  The call a reference-side binding makes
+   for a list of gfp_mul_fft / gfp_mul_bigint products (bench_cli bench-mul,
+   bench_cli.py:282-324). */
+int gfp_vec_mul_host(const uint64_t *x, const uint64_t *y, uint64_t *z, int64_t n, int k,
+                     uint64_t r, void *stream);
+
 /* z = x * y mod p through the reference's own mechanism (gfp_mul_fft,
    gfp_mult.py:416-501, paper Alg. 13): negacyclic convolutions of the digit
    vectors over the word primes P1, P2 (theta-weighted NTTs in Montgomery
@@ -256,6 +264,14 @@ int gfp_fft_plan_caps(const gfp_fft_plan *plan);
    GFP_E* on failure).  Off by default: no events, no overhead. */
 int gfp_fft_plan_set_timing(gfp_fft_plan *plan, int on);
 int gfp_fft_plan_pass_times(gfp_fft_plan *plan, float *ms, int *pass, int max);
+
+/* 1 in the checked build (GFP_DEBUG: index guards + timing jitter in the
+   pass / exchange kernels, the stand-in for compute-sanitizer), else 0.
+   gfp_debug_selftest launches one kernel that performs a deliberately
+   out-of-range guarded index, so a checked build prints its GFP_CHECK line
+   (proving the guards are live); GFP_EUNSUPPORTED in the product build. */
+int gfp_debug_build(void);
+int gfp_debug_selftest(void *stream);
 
 /* Instrumentation: run `iters` x 8 independent IMAD.WIDE (32x32 -> 64)
    product chains per thread on a blocks x threads grid and report the kernel time and the

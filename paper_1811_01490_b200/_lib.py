@@ -38,6 +38,7 @@ SIGNATURES = {
     "gfp_vec_sub": (_int, [_u64p, _u64p, _u64p, _i64, _int, _u64, _vp]),
     "gfp_vec_mul_pow_r": (_int, [_u64p, _u64p, _i64, _int, _u64, _int, _vp]),
     "gfp_vec_mul": (_int, [_u64p, _u64p, _i64, _u64p, _i64, _int, _u64, _vp]),
+    "gfp_vec_mul_host": (_int, [_u64p, _u64p, _u64p, _i64, _int, _u64, _vp]),
     "gfp_vec_mul_crt": (_int, [_u64p, _u64p, _i64, _u64p, _i64, _int, _u64, _vp]),
     "gfp_vec_mul_crt_profile": (_int, [_u64p, _u64p, _i64, _u64p, _i64, _int, _u64,
                                        ctypes.POINTER(ctypes.c_uint64),
@@ -80,6 +81,8 @@ SIGNATURES = {
     "gfp_ipc_get_handle": (_int, [_vp, ctypes.c_char_p, ctypes.POINTER(_i64)]),
     "gfp_ipc_open": (_int, [ctypes.c_char_p, _i64, ctypes.POINTER(_vp)]),
     "gfp_ipc_close": (_int, [_vp, _i64]),
+    "gfp_debug_build": (_int, []),
+    "gfp_debug_selftest": (_int, [_vp]),
     "gfp_probe_imad_wide": (_int, [_i64, _int, _int, ctypes.POINTER(ctypes.c_float),
                                    ctypes.POINTER(ctypes.c_double), _vp]),
 }

@@ -33,6 +33,42 @@ typedef __int128 i128;
 #define GFP_HD __host__ __device__ __forceinline__
 #define GFP_D __device__ __forceinline__
 
+// ---------------------------------------------------------------------------
+// Checked build (make checked: GFP_DEBUG=1).  compute-sanitizer is not
+// available on the GPU pool, so the library checks itself: GFP_IDX(i, n)
+// guards every global / shared index of the pass and exchange kernels
+// against the logical extent of the buffer it addresses (a violation prints
+// "GFP_CHECK <file>:<line> idx lim" and redirects the access to index 0, so
+// the result is also wrong and the oracle comparison fails), and
+// GFP_JITTER(site) sleeps a pseudo-random few hundred ns per warp at phase
+// boundaries -- perturbing the warps' relative timing so that a missing
+// barrier shows up as a wrong result (a timing-perturbation race test).
+// Both compile to nothing in the product build.
+#ifndef GFP_DEBUG
+#define GFP_DEBUG 0
+#endif
+#if GFP_DEBUG
+#include <stdio.h>
+static __device__ __noinline__ long long gfp_idx_fail(long long idx, long long lim, const char *file,
+                                               int line)
+{
+    printf("GFP_CHECK %s:%d idx=%lld lim=%lld block=(%d,%d) thread=%d\n", file, line, idx, lim,
+           (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x);
+    return 0;
+}
+#define GFP_IDX(idx, lim)                                                                       \
+    ([&]() -> long long {                                                                       \
+        const long long i_ = (long long)(idx), l_ = (long long)(lim);                           \
+        return (i_ < 0 || i_ >= l_) ? gfp_idx_fail(i_, l_, __FILE__, __LINE__) : i_;            \
+    }())
+#define GFP_JITTER(site)                                                                        \
+    __nanosleep((unsigned)(((blockIdx.x * 131u + blockIdx.y * 7919u + (threadIdx.x >> 5) * 97u + \
+                             (site) * 2654435761u) >> 7) & 511u))
+#else
+#define GFP_IDX(idx, lim) (idx)
+#define GFP_JITTER(site) ((void)0)
+#endif
+
 // Per-radix constants, computed once on the host (exact integer arithmetic in
 // the Python plan code) and passed by value to every kernel.
 struct RadixConsts {

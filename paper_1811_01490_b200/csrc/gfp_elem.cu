@@ -407,6 +407,68 @@ __global__ void k_transpose(const u64 *__restrict__ src, u64 *__restrict__ dst, 
     }
 }
 
+// Batched, tiled layout conversion between element-major [B][n_em][k] and
+// digit-major [B][k][n_dm] (the host entry points' staging): a CTA moves
+// tiles of 32 elements x k digits through shared memory, so both the
+// element-major side (32 k contiguous words) and every digit row (32
+// contiguous words) are accessed coalesced.  to_dm: element-major -> digit-
+// major, elements i >= n_em written as 0 (zero padding to the transform
+// length); otherwise digit-major -> element-major for i < n_em (truncation
+// to the product length).  n_dm >= n_em.
+template <int KD>
+__global__ void __launch_bounds__(256) k_transpose_tiles(const u64 *__restrict__ src,
+                                                         u64 *__restrict__ dst, int64_t batch,
+                                                         int64_t n_em, int64_t n_dm, int to_dm)
+{
+    __shared__ u64 tile[32 * (KD + 1)];
+    const int64_t tiles_per = (n_dm + 31) / 32;
+    const int64_t ntiles = batch * tiles_per;
+    for (int64_t tt = blockIdx.x; tt < ntiles; tt += gridDim.x) {
+        const int64_t b = tt / tiles_per;
+        const int64_t i0 = (tt - b * tiles_per) * 32;
+        if (!to_dm && i0 >= n_em)
+            continue;
+        const u64 *s_em = src + b * n_em * KD;  // element-major side (to_dm)
+        const u64 *s_dm = src + b * n_dm * KD;  // digit-major side (!to_dm)
+        u64 *d_em = dst + b * n_em * KD;
+        u64 *d_dm = dst + b * n_dm * KD;
+        __syncthreads();
+        for (int w = threadIdx.x; w < 32 * KD; w += blockDim.x) {
+            if (to_dm) {  // w = e k + d over the 32 elements' contiguous words
+                const int e = w / KD, d = w % KD;
+                tile[e * (KD + 1) + d] = i0 + e < n_em ? s_em[(i0 + e) * KD + d] : 0;
+            } else {      // w = d 32 + e: digit rows
+                const int d = w / 32, e = w % 32;
+                tile[e * (KD + 1) + d] = i0 + e < n_dm ? s_dm[(int64_t)d * n_dm + i0 + e] : 0;
+            }
+        }
+        __syncthreads();
+        for (int w = threadIdx.x; w < 32 * KD; w += blockDim.x) {
+            if (to_dm) {
+                const int d = w / 32, e = w % 32;
+                if (i0 + e < n_dm)
+                    d_dm[(int64_t)d * n_dm + i0 + e] = tile[e * (KD + 1) + d];
+            } else {
+                const int e = w / KD, d = w % KD;
+                if (i0 + e < n_em)
+                    d_em[(i0 + e) * KD + d] = tile[e * (KD + 1) + d];
+            }
+        }
+    }
+}
+
+int transpose_batched(const u64 *src, u64 *dst, int64_t batch, int64_t n_em, int64_t n_dm, int k,
+                      int to_dm, cudaStream_t st)
+{
+    if (batch <= 0 || n_dm <= 0)
+        return GFP_OK;
+    const int64_t tiles = batch * ((n_dm + 31) / 32);
+    const int64_t cap = (int64_t)num_sms() * 8;
+    const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
+    DISPATCH_K(k, (k_transpose_tiles<KD><<<grid, 256, 0, st>>>(src, dst, batch, n_em, n_dm, to_dm)));
+    return cuda_status();
+}
+
 static int g_num_sms[64];  // per device id (0 = not queried yet)
 
 int num_sms()
@@ -601,6 +663,41 @@ int gfp_vec_uniform(uint64_t *z, int64_t n, int k, uint64_t r, uint64_t seed, vo
         return e;
     k_uniform<<<grid_for(n * k, 256), 256, 0, (cudaStream_t)stream>>>(z, n, k, r, seed);
     return cuda_status();
+}
+
+int gfp_vec_mul_host(const uint64_t *x, const uint64_t *y, uint64_t *z, int64_t n, int k,
+                     uint64_t r, void *stream)
+{
+    int e = check_kr(k, r);
+    if (e)
+        return e;
+    if (!x || !y || !z || n < 0)
+        return GFP_EINVAL;
+    if (n == 0)
+        return GFP_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t words = (size_t)n * k;
+    u64 *buf = nullptr;
+    if (cudaMallocAsync(&buf, 4 * words * sizeof(u64), st) != cudaSuccess) {
+        cudaGetLastError();
+        return GFP_ENOMEM;
+    }
+    u64 *hx = buf, *hy = buf + words, *dx = buf + 2 * words, *dy = buf + 3 * words;
+    cudaMemcpyAsync(hx, x, words * sizeof(u64), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(hy, y, words * sizeof(u64), cudaMemcpyHostToDevice, st);
+    e = transpose_batched(hx, dx, 1, n, n, k, 1, st);
+    if (!e)
+        e = transpose_batched(hy, dy, 1, n, n, k, 1, st);
+    if (!e)
+        e = gfp_vec_mul(dx, dy, 1, dx, n, k, r, st);
+    if (!e)
+        e = transpose_batched(dx, hx, 1, n, n, k, 0, st);
+    if (!e)
+        cudaMemcpyAsync(z, hx, words * sizeof(u64), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(buf, st);
+    if (!e && cudaStreamSynchronize(st) != cudaSuccess)
+        e = GFP_ECUDA;
+    return e ? e : cuda_status();
 }
 
 int gfp_to_digit_major(const uint64_t *src, uint64_t *dst, int64_t n, int k, void *stream)

@@ -45,12 +45,12 @@ __global__ void __launch_bounds__(TA *TY) k_exchange(const uint64_t *__restrict_
     for (int i = 0; i < TA / TY; i++) {
         const int64_t a = a0 + ty + TY * i;
         if (a < A) {
-            const uint64_t *row = src + (a * k + d) * B;
 #pragma unroll
             for (int h = 0; h < TB / 32; h++) {
                 const int64_t bc = b0 + tx + 32 * h;
                 if (bc < B)
-                    tile[ty + TY * i][tx + 32 * h] = __ldcs(row + bc);
+                    tile[ty + TY * i][tx + 32 * h] =
+                        __ldcs(src + GFP_IDX((a * k + d) * B + bc, A * k * B));
             }
         }
     }
@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(TA *TY) k_exchange(const uint64_t *__restrict_
             v = tid == q ? dst.p[q] : v;
         sdst[tid] = v;
     }
+    GFP_JITTER(1);
     __syncthreads();
     // write: for column bc = b0 + j (j = ty + TY i), 32 consecutive a; the
     // owner g and local index bl advance incrementally (one division per
@@ -84,7 +85,9 @@ __global__ void __launch_bounds__(TA *TY) k_exchange(const uint64_t *__restrict_
             }
         }
         if (b0 + j < B && a < A)
-            __stcs(sdst[g] + (bl * k + d) * GA + (int64_t)rank * A + a, tile[tx][j]);
+            __stcs(sdst[GFP_IDX(g, G)] + GFP_IDX((bl * k + d) * GA + (int64_t)rank * A + a,
+                                                   b * k * GA),
+                   tile[tx][j]);
     }
 }
 

@@ -19,6 +19,10 @@ int num_sms();
 dim3 grid_for(int64_t work, int threads);
 int cuda_status();
 int check_kr(int k, u64 r);
+// element-major [B][n_em][k] <-> digit-major [B][k][n_dm] (to_dm: zero-pad
+// i >= n_em; else write i < n_em only), tiled through shared memory
+int transpose_batched(const u64 *src, u64 *dst, int64_t batch, int64_t n_em, int64_t n_dm, int k,
+                      int to_dm, cudaStream_t st);
 
 // Run f once per CUDA device (function attributes such as the dynamic
 // shared-memory limit apply per device context); `mask` holds one bit per

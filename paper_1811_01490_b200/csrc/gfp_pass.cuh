@@ -188,7 +188,8 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
             const unsigned rowN = 1u << lN;
 #pragma unroll
             for (int d = 0; d < KD; d++)
-                x[d] = (i64)__ldg(src + (size_t)((unsigned)((d - as) & (KD - 1)) * rowN));
+                x[d] = (i64)__ldg(src + GFP_IDX((size_t)((unsigned)((d - as) & (KD - 1)) * rowN),
+                                                (int64_t)KD * N - pos));
             if (A.in_canon)  // pass 0 only, where a = 0
                 to_balanced<KD>(x, rc.r);
             if (!NOMUL && pre) {  // pass 0 only (a = b = 0)
@@ -202,7 +203,8 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
 #pragma unroll
                     for (int d = 0; d < KD; d++) {
                         int l, h;
-                        split_limbs<S>((i64)__ldg(pre + ((int64_t)d << lN) + pos), l, h);
+                        split_limbs<S>((i64)__ldg(pre + GFP_IDX(((int64_t)d << lN) + pos,
+                                                                (int64_t)KD << lN)), l, h);
                         yw[d * nt] = (u64)(unsigned)l | ((u64)(unsigned)h << 32);
                     }
                     i64 *prow = sm + (((int64_t)t << lG) + g) * ROW;
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
                     i64 y[KD];
 #pragma unroll
                     for (int d = 0; d < KD; d++)
-                        y[d] = (i64)__ldg(pre + ((int64_t)d << lN) + pos);
+                        y[d] = (i64)__ldg(pre + GFP_IDX(((int64_t)d << lN) + pos, (int64_t)KD << lN));
                     fast_mul_lazy<KD, SPARSE>(x, y, x, rc);
                 }
             }
@@ -228,7 +230,8 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
         // warp-uniform multiply: lanes with b = 0 multiply by table[0] = 1
         if (!NOMUL && __any_sync(FULL_MASK, active && (b || A.scale))) {
             if (active) {
-                const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(A.table_lh + b * KD);
+                const ulonglong2 *tp =
+                    reinterpret_cast<const ulonglong2 *>(A.table_lh + GFP_IDX(b, M) * KD);
                 if (PASS_WINDOW(KD)) {
                     // twiddle limbs staged in this thread's smem column,
                     // multiplied through the sliding window (registers: x only)
@@ -266,6 +269,7 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
                 row[d] = ((negx >> d) & 1u) ? -x[d] : x[d];
         }
     }
+    GFP_JITTER(1);
     __syncthreads();
 
     // ---- phase B: K-point DFT at root r (or 1/r), one digit per lane
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
         i64 v[K];
 #pragma unroll
         for (int t = 0; t < K; t++)
-            v[t] = sm[(((int64_t)t << lG) + g) * ROW + d];
+            v[t] = sm[GFP_IDX((((int64_t)t << lG) + g) * ROW + d, ((int64_t)K << lG) * ROW)];
         const int S = rc.stages_per_norm;
         int stage = 0;
 #pragma unroll
@@ -342,8 +346,10 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
         __syncthreads();
 #pragma unroll
         for (int t = 0; t < K; t++)
-            sm[(((int64_t)bitrev_c<K>(t) << lG) + g) * ROW + d] = v[t];
+            sm[GFP_IDX((((int64_t)bitrev_c<K>(t) << lG) + g) * ROW + d,
+                       ((int64_t)K << lG) * ROW)] = v[t];
     }
+    GFP_JITTER(2);
     __syncthreads();
 
     // ---- phase C: store in Stockham order (canonicalise on the last pass)
@@ -367,11 +373,11 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
             lazy_to_canonical_bf<KD>(f, c, rc);  // balanced digits (phase B)
 #pragma unroll
             for (int d = 0; d < KD; d++)
-                out[((int64_t)d << lN) + pos] = c[d];
+                out[GFP_IDX(((int64_t)d << lN) + pos, (int64_t)KD << lN)] = c[d];
         } else {
 #pragma unroll
             for (int d = 0; d < KD; d++)
-                out[((int64_t)d << lN) + pos] = (u64)row[d];
+                out[GFP_IDX(((int64_t)d << lN) + pos, (int64_t)KD << lN)] = (u64)row[d];
         }
     }
 }

@@ -232,12 +232,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
     u64 *stg = pf_stage + w * (KD * 32) + lane;
     auto prefetch = [&](int i) {
         if (active) {
-            const u64 *src = in + j + ((int64_t)(w + NW * i) << lM);
+            const int64_t e0 = j + ((int64_t)(w + NW * i) << lM);
 #pragma unroll
             for (int r_ = 0; r_ < KD; r_++) {
                 const unsigned sa = (unsigned)__cvta_generic_to_shared(stg + r_ * 32);
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa),
-                             "l"(src + ((int64_t)r_ << lN))
+                             "l"(in + GFP_IDX(e0 + ((int64_t)r_ << lN), (int64_t)KD << lN))
                              : "memory");
             }
         }
@@ -257,14 +257,15 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
             // host memory: the warp's 32 elements (j0 .. j0 + 31, t) are 2 KB
             // contiguous; read them with lane-contiguous 16 B loads (full
             // 512 B requests over PCIe) into this row's smem slots
-            const u64 *rowp = em_in + (j0 + ((int64_t)t << lM)) * KD;
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 const int e = (lane >> 2) + 8 * q, dp = (lane & 3) * 2;
                 ulonglong2 v = make_ulonglong2(0, 0);
                 if (e < gpc && j0 + e < M && j0 + e + ((int64_t)t << lM) < n_in)
-                    v = reinterpret_cast<const ulonglong2 *>(rowp)[lane + 32 * q];
-                *reinterpret_cast<ulonglong2 *>(sm + (t * 32 + e) * SLOT + dp) = v;
+                    v = reinterpret_cast<const ulonglong2 *>(
+                        em_in)[GFP_IDX(((j0 + ((int64_t)t << lM)) * KD) / 2 + lane + 32 * q,
+                                       n_in * KD / 2)];
+                *reinterpret_cast<ulonglong2 *>(sm + GFP_IDX((t * 32 + e) * SLOT + dp, (K * 32 * SLOT))) = v;
             }
             __syncwarp();
         }
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
             b = tw.b;
             negx = tw.negx;
             if (em_in) {
-                const i64 *slot = sm + (t * 32 + lane) * SLOT;
+                const i64 *slot = sm + GFP_IDX((t * 32 + lane) * SLOT, (K * 32 * SLOT));
 #pragma unroll
                 for (int d = 0; d < KD; d += 2) {
                     const longlong2 v = *reinterpret_cast<const longlong2 *>(slot + d);
@@ -308,14 +309,15 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
                 const unsigned rowN = 1u << lN;
 #pragma unroll
                 for (int d = 0; d < KD; d++)  // streamed once: evict-first, keep the tables in L2
-                    x[d] = (i64)__ldcs(src + (unsigned)((d - tw.as) & (KD - 1)) * rowN);
+                    x[d] = (i64)__ldcs(src + GFP_IDX((unsigned)((d - tw.as) & (KD - 1)) * rowN,
+                                                     (int64_t)KD * N - pos));
             }
             if (A.in_canon)  // pass 0 only, where a = 0
                 to_balanced<KD>(x, rc.r);
         }
         // element t parks in slot t: holding four elements in registers
         // across the multiplies would cost occupancy
-        i64 *slot = sm + (t * 32 + lane) * SLOT;
+        i64 *slot = sm + GFP_IDX((t * 32 + lane) * SLOT, (K * 32 * SLOT));
         // Up to two multiplies through ONE inlined copy of the multiply (the
         // kernel's code size matters: ~2/3 of it would be multiplies): the
         // pointwise product by `pre` (pass 0 only, a = b = 0), then the
@@ -343,12 +345,14 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
 #pragma unroll
                     for (int d = 0; d < KD; d++) {
                         int l, h;
-                        split_limbs<S>((i64)__ldg(pre + ((int64_t)d << lN) + pos), l, h);
+                        split_limbs<S>((i64)__ldg(pre + GFP_IDX(((int64_t)d << lN) + pos,
+                                                                (int64_t)KD << lN)), l, h);
                         ylh[d] = (u64)(unsigned)l | ((u64)(unsigned)h << 32);
                     }
                 } else {
                     const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(
-                        (A.ft_lh ? A.ft_lh : A.table_lh) + b * KD);
+                        (A.ft_lh ? A.ft_lh : A.table_lh) +
+                        GFP_IDX(b, A.ft_lh ? ((int64_t)1 << A.ft_lM) : M) * KD);
 #pragma unroll
                     for (int d = 0; d < KD; d += 2) {
                         const ulonglong2 v = __ldg(tp + d / 2);
@@ -378,6 +382,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
         }
     }
 
+    GFP_JITTER(1);
     // ---- stage 1 (warps w < 4, t1 = w): 4-point DFT over t2 (root rho^4) of
     // slots t1 + 4 t2, outputs u0 = 0..3 back into slots t1 + 4 u0 (the same
     // slots: no other thread touches them).  With NW = 4 the thread reads
@@ -387,7 +392,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
     if (w < 4) {
 #pragma unroll
     for (int t2 = 0; t2 < 4; t2++) {
-        const i64 *slot = sm + ((t2 * 4 + w) * 32 + lane) * SLOT;
+        const i64 *slot = sm + GFP_IDX(((t2 * 4 + w) * 32 + lane) * SLOT, (K * 32 * SLOT));
 #pragma unroll
         for (int d = 0; d < KD; d += 2) {
             const longlong2 v = *reinterpret_cast<const longlong2 *>(slot + d);
@@ -398,12 +403,13 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
     p44::dft4<KD, INV, 0>(e[0], e[1], e[2], e[3]);
 #pragma unroll
     for (int u0 = 0; u0 < 4; u0++) {
-        i64 *slot = sm + ((u0 * 4 + w) * 32 + lane) * SLOT;
+        i64 *slot = sm + GFP_IDX(((u0 * 4 + w) * 32 + lane) * SLOT, (K * 32 * SLOT));
 #pragma unroll
         for (int d = 0; d < KD; d += 2)
             *reinterpret_cast<longlong2 *>(slot + d) = make_longlong2(e[u0][d], e[u0][d + 1]);
     }
     }
+    GFP_JITTER(2);
     __syncthreads();
     // Stage 2 over SPL = NW / 4 warps per u0 (P44_SPLIT2): every warp gathers
     // its u0's four slots and computes the (cheap, lazy) 4-point DFT, then
@@ -419,7 +425,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
     // ---- stage 2: gather Y[t1][u0], twiddle rho^(t1 u0), DFT over t1
 #pragma unroll
     for (int t1 = 0; t1 < 4; t1++) {
-        const i64 *slot = sm + ((u0 * 4 + t1) * 32 + lane) * SLOT;
+        const i64 *slot = sm + GFP_IDX(((u0 * 4 + t1) * 32 + lane) * SLOT, (K * 32 * SLOT));
 #pragma unroll
         for (int d = 0; d < KD; d += 2) {
             const longlong2 v = *reinterpret_cast<const longlong2 *>(slot + d);
@@ -466,12 +472,13 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
         // possibly mapped host memory: park the canonical outputs in the
         // stage-2 slots (rows 4 u0 + u1), then write each u's 32 elements
         // (2 KB contiguous) with lane-contiguous 16 B stores
+        GFP_JITTER(3);
         if (SPL > 1)  // the u0 slots are read by every warp of the u0 above
             asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
 #pragma unroll
         for (int q = 0; q < NU; q++) {
             const int u1 = h * NU + q;
-            i64 *slot = sm + ((4 * u0 + u1) * 32 + lane) * SLOT;
+            i64 *slot = sm + GFP_IDX(((4 * u0 + u1) * 32 + lane) * SLOT, (K * 32 * SLOT));
 #pragma unroll
             for (int d = 0; d < KD; d += 2)
                 *reinterpret_cast<longlong2 *>(slot + d) = make_longlong2(e[q][d], e[q][d + 1]);
@@ -481,14 +488,15 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
         for (int q = 0; q < NU; q++) {
             const int u1 = h * NU + q;
             const int64_t ubase = j0 + ((int64_t)(u0 + 4 * u1) << lM);
-            u64 *rowp = em_out + ubase * KD;
 #pragma unroll
             for (int qq = 0; qq < 4; qq++) {
                 const int e = (lane >> 2) + 8 * qq, dp = (lane & 3) * 2;
                 const longlong2 v =
-                    *reinterpret_cast<const longlong2 *>(sm + ((4 * u0 + u1) * 32 + e) * SLOT + dp);
+                    *reinterpret_cast<const longlong2 *>(
+                        sm + GFP_IDX(((4 * u0 + u1) * 32 + e) * SLOT + dp, (K * 32 * SLOT)));
                 if (e < gpc && j0 + e < M && ubase + e < A.n_out)
-                    reinterpret_cast<ulonglong2 *>(rowp)[lane + 32 * qq] =
+                    reinterpret_cast<ulonglong2 *>(
+                        em_out)[GFP_IDX(ubase * KD / 2 + lane + 32 * qq, A.n_out * KD / 2)] =
                         make_ulonglong2((u64)v.x, (u64)v.y);
             }
         }
@@ -502,13 +510,14 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
         // positions lane-contiguously.
         constexpr int NT = SPL * 128;  // threads in stage 2
         i64 *park = sm;
+        GFP_JITTER(4);
         asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");  // stage-2 slot reads done
 #pragma unroll
         for (int q = 0; q < NU; q++) {
             const int u = u0 + 4 * (h * NU + q);
 #pragma unroll
             for (int d = 0; d < KD; d++)
-                park[(d * 32 + lane) * 17 + u] = e[q][d];
+                park[GFP_IDX((d * 32 + lane) * 17 + u, (K * 32 * SLOT))] = e[q][d];
         }
         asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
         const int tid = threadIdx.x;  // < NT: the stage-2 warps
@@ -520,7 +529,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
             if (g < gpc && j0 + g < M) {
 #pragma unroll
                 for (int d = 0; d < KD; d++)
-                    __stcs(obase + ((int64_t)d << lN) + q, (u64)park[(d * 32 + g) * 17 + u]);
+                    __stcs(obase + GFP_IDX(((int64_t)d << lN) + q, ((int64_t)KD << lN) - (j0 << 4)),
+                           (u64)park[GFP_IDX((d * 32 + g) * 17 + u, (K * 32 * SLOT))]);
             }
         }
         return;
@@ -541,10 +551,12 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
 #pragma unroll
             for (int gg = 1; gg < 8; gg++)
                 dp = g == gg ? A.xdst[gg] : dp;
+            (void)GFP_IDX(g, A.xg);
             dp += (pos & bmask) * KD * GA + col;
 #pragma unroll
             for (int d = 0; d < KD; d++)
-                __stcs(dp + d * GA, (u64)e[q][d]);
+                __stcs(dp + GFP_IDX(d * GA, ((bmask + 1) * KD - (pos & bmask) * KD) * GA - col),
+                       (u64)e[q][d]);
         }
         return;
     }
@@ -553,7 +565,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? (XCH ? P44_XCH_MINB : P44_M
         const int64_t pos = base + ((int64_t)(u0 + 4 * (h * NU + q)) << lNs);
 #pragma unroll
         for (int d = 0; d < KD; d++)
-            __stcs(out + ((int64_t)d << lN) + pos, (u64)e[q][d]);
+            __stcs(out + GFP_IDX(((int64_t)d << lN) + pos, (int64_t)KD << lN), (u64)e[q][d]);
     }
 }
 

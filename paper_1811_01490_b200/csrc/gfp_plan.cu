@@ -614,36 +614,35 @@ static u64 *mapped_alias(const void *h)
     return nullptr;
 }
 
-// the staged route for kernels without element-major I/O (k != 8): zero-pad
-// into digit-major device vectors, transform, transpose back
+// the staged route for kernels without element-major I/O (k != 8): one copy
+// of each operand's nf / ng elements, one batched transpose that zero-pads to
+// N, the product, one batched transpose of its first n_out elements, one copy
+// back -- O(1) copies and launches per call, whatever the batch
 static int poly_mul_host_staged(gfp_fft_plan *p, const u64 *f, int64_t nf, const u64 *g,
                                 int64_t ng, u64 *out, int64_t n_out, int64_t batch,
                                 cudaStream_t st)
 {
     const int k = p->k;
     const int64_t N = p->N, vw = (int64_t)k * N * batch;
-    int err = ensure_host_scratch(p, 7 * vw);
+    int err = ensure_host_scratch(p, 7 * vw);  // staging, operands, poly_mul workspace (3 vw)
     if (err)
         return err;
     u64 *hf = p->h_dev, *hg = hf + vw, *df = hg + vw, *dg = df + vw, *w = dg + vw;
-    cudaMemsetAsync(hf, 0, sizeof(u64) * 2 * vw, st);
-    for (int64_t i = 0; i < batch; i++) {
-        cudaMemcpyAsync(hf + i * k * N, f + i * k * nf, sizeof(u64) * k * nf,
-                        cudaMemcpyHostToDevice, st);
-        cudaMemcpyAsync(hg + i * k * N, g + i * k * ng, sizeof(u64) * k * ng,
-                        cudaMemcpyHostToDevice, st);
-        gfp_to_digit_major(hf + i * k * N, df + i * k * N, N, k, st);
-        gfp_to_digit_major(hg + i * k * N, dg + i * k * N, N, k, st);
-    }
-    err = gfp_poly_mul(p, df, dg, df, w, batch, st);
+    cudaMemcpyAsync(hf, f, sizeof(u64) * k * nf * batch, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(hg, g, sizeof(u64) * k * ng * batch, cudaMemcpyHostToDevice, st);
+    err = transpose_batched(hf, df, batch, nf, N, k, 1, st);
+    if (!err)
+        err = transpose_batched(hg, dg, batch, ng, N, k, 1, st);
+    if (!err)
+        err = gfp_poly_mul(p, df, dg, df, w, batch, st);
     if (err)
         return err;
-    for (int64_t i = 0; i < batch; i++) {
-        gfp_to_element_major(df + i * k * N, hf + i * k * N, N, k, st);
-        cudaMemcpyAsync(out + i * k * n_out, hf + i * k * N, sizeof(u64) * k * n_out,
-                        cudaMemcpyDeviceToHost, st);
-    }
-    p->last_launches += 3 * batch;
+    const int64_t launches = p->last_launches;
+    err = transpose_batched(df, hf, batch, n_out, N, k, 0, st);
+    if (err)
+        return err;
+    cudaMemcpyAsync(out, hf, sizeof(u64) * k * n_out * batch, cudaMemcpyDeviceToHost, st);
+    p->last_launches = launches + 3;
     return GFP_OK;
 }
 
@@ -737,16 +736,16 @@ int gfp_fft_exec_host(gfp_fft_plan *p, uint64_t *v, int64_t batch, int inverse, 
         src = stg;
     }
     if (!em_io_supported(p)) {
-        // no element-major kernel for this k: transpose around the transform
-        cudaMemcpyAsync(a, src, sizeof(u64) * vw, cudaMemcpyDeviceToDevice, st);
-        for (int64_t i = 0; i < batch; i++)
-            gfp_to_digit_major(a + i * k * N, b + i * k * N, N, k, st);
-        err = run_transform(p, b, b, w, nullptr, batch, inverse ? 1 : 0, 1, 1, st);
+        // no element-major kernel for this k: one batched transpose on each
+        // side of the transform
+        err = transpose_batched(src, b, batch, N, N, k, 1, st);
+        if (!err)
+            err = run_transform(p, b, b, w, nullptr, batch, inverse ? 1 : 0, 1, 1, st);
+        if (!err)
+            err = transpose_batched(b, a, batch, N, N, k, 0, st);
         if (err)
             return err;
-        for (int64_t i = 0; i < batch; i++)
-            gfp_to_element_major(b + i * k * N, a + i * k * N, N, k, st);
-        p->last_launches += 2 * batch;
+        p->last_launches += 2;
         cudaMemcpyAsync(v, a, sizeof(u64) * vw, cudaMemcpyDeviceToHost, st);
     } else {
         PassIO em = {src, nullptr, N, 0, stage_out ? a : mv, N, nullptr, 0, 0};

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include "gfpfft.h"
+#include "gfp_internal.cuh"
 
 #define NCH 8
 
@@ -65,4 +66,26 @@ extern "C" int gfp_probe_imad_wide(int64_t iters, int blocks, int threads, float
     *ms_out = ms;
     *ops_out = (double)blocks * threads * (double)iters * NCH;
     return cudaGetLastError() == cudaSuccess ? GFP_OK : GFP_ECUDA;
+}
+
+// ---- the checked build's self-test (gfp_debug_build / gfp_debug_selftest)
+__global__ void k_debug_selftest(uint64_t *out, int64_t lim)
+{
+    // one guarded index past its extent: the checked build prints GFP_CHECK
+    out[GFP_IDX(lim + threadIdx.x, lim)] = 1;
+}
+
+extern "C" int gfp_debug_build(void) { return GFP_DEBUG; }
+
+extern "C" int gfp_debug_selftest(void *stream)
+{
+    if (!GFP_DEBUG)
+        return GFP_EUNSUPPORTED;
+    uint64_t *buf = nullptr;
+    if (cudaMalloc(&buf, 4 * sizeof(uint64_t)) != cudaSuccess)
+        return GFP_ENOMEM;
+    k_debug_selftest<<<1, 1, 0, (cudaStream_t)stream>>>(buf, 4);
+    const int err = cudaStreamSynchronize((cudaStream_t)stream) == cudaSuccess ? GFP_OK : GFP_ECUDA;
+    cudaFree(buf);
+    return err;
 }

@@ -92,6 +92,21 @@ def mul(x, y, params):
     return z
 
 
+def mul_host(x, y, params):
+    """Element-wise product of element-major host arrays [n, k] (uint64) ->
+    new [n, k] array (gfp_vec_mul_host: the whole H2D / multiply / D2H)."""
+    import ctypes as C
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.uint64))
+    y = np.ascontiguousarray(np.asarray(y, dtype=np.uint64))
+    if x.shape != y.shape or x.ndim != 2 or x.shape[1] != params.k:
+        raise ValueError("operands must be [n, k] arrays of the same shape")
+    z = np.empty_like(x)
+    _lib.check(_lib.load().gfp_vec_mul_host(C.c_void_p(x.ctypes.data), C.c_void_p(y.ctypes.data),
+                                           C.c_void_p(z.ctypes.data), x.shape[0], params.k,
+                                           params.r, _stream()), "gfp_vec_mul_host")
+    return z
+
+
 def mul_crt(x, y, params):
     """Element-wise product through the reference's own mechanism (two word-
     prime negacyclic convolutions, CRT, LHC: gfp_mul_fft, gfp_mult.py:416-501);
