@@ -715,6 +715,29 @@ def multi_gpu_configs(args, ws, rank, dev, flush, stream):
     return res
 
 
+def _pinned_em(gp, x):
+    """Digit-major device vectors [B, k, N] (or [k, N]) -> a pinned host
+    element-major uint64 array [B, N, k] (or [N, k]) holding the same values."""
+    import numpy as np
+    import torch
+    xs = x if x.dim() == 3 else x.unsqueeze(0)
+    B, k, N = xs.shape
+    t = torch.empty((B, N, k), dtype=torch.int64).pin_memory()
+    v = t.numpy().view(np.uint64)
+    for b in range(B):
+        v[b] = gp.vec.to_host(xs[b])
+    return (v if x.dim() == 3 else v[0]), t
+
+
+def e2e_entry(fn, steps, flush, stream, elements, h2d, d2h, api):
+    """The config's metric through a host-buffer entry point, H2D and D2H
+    inside the timed region (the call is synchronous)."""
+    t = timed_loop(fn, max(3, steps // 2), 1, 1, flush, stream)
+    ms = sum(t) / len(t)
+    return {"ms_per_step": ms, "elements_per_s": elements / (ms * 1e-3),
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": api}
+
+
 def extra_configs(args, dev, flush, stream, hbm_peak, imad_peak):
     """The other BASELINE.json configs, timed briefly (elements/s)."""
     import torch
@@ -739,6 +762,15 @@ def extra_configs(args, dev, flush, stream, hbm_peak, imad_peak):
                 t = timed_loop(step, steps, 2, 1, flush, stream)
                 ms = sum(t) / len(t)
                 entry.update(ms_fwd_plus_inv=ms, elements_per_s=N / (ms * 1e-3))
+                xh, keep = _pinned_em(gp, x)
+
+                def e2e():
+                    gp.fft_host(xh, plan, inplace=True)
+                    gp.fft_host(xh, plan, inverse=True, inplace=True)
+                entry["e2e"] = e2e_entry(e2e, steps, flush, stream, N, 2 * N * k * 8, 2 * N * k * 8,
+                                         "gfp_fft_exec_host forward + inverse, pinned "
+                                         "element-major [2^12, 8] in place (zero-copy)")
+                del xh, keep
             elif key in ("c3", "c4"):
                 def step():
                     gp.fft_tensor(x, plan, out=y)
@@ -750,6 +782,19 @@ def extra_configs(args, dev, flush, stream, hbm_peak, imad_peak):
                              tera_imad_executed_per_s=mults * 3 * k * k / (ms * 1e-3) / 1e12)
                 entry["passes"] = pass_roofline(gp, plan, step, k, N, K, B, "fwd", hbm_peak,
                                                 imad_peak, reps=3)
+                # e2e: element-major pinned host vectors through the host entry
+                # point (C3: a sample of 8 of the 64 transforms, 1 GiB)
+                Be = min(B, 8)
+                xh, keep = _pinned_em(gp, x[:Be] if B > 1 else x)
+                nbytes = Be * N * k * 8
+                entry["e2e"] = e2e_entry(
+                    lambda: gp.fft_host(xh, plan, inplace=True), steps, flush, stream, Be * N,
+                    nbytes, nbytes,
+                    "gfp_fft_exec_host, pinned element-major [%d, 2^%d, %d] in place (%s)" % (
+                        Be, N.bit_length() - 1, k,
+                        "zero-copy first/last pass" if k == 8 else
+                        "one DMA copy each way + batched tiled transposes"))
+                del xh, keep
             else:
                 n = 1 << 22
                 a = gp.vec.uniform(n, params, seed=51)
@@ -770,12 +815,27 @@ def extra_configs(args, dev, flush, stream, hbm_peak, imad_peak):
                 t = timed_loop(cstep, max(3, steps // 2), 2, 1, flush, stream)
                 ms = sum(t) / len(t)
                 entry.update(ms_mul_mechanism=ms, mechanism_muls_per_s=n / (ms * 1e-3))
+                # e2e: the 2^22 pairs as element-major pinned host arrays
+                ah, ka = _pinned_em(gp, a)
+                bh, kb = _pinned_em(gp, b)
+                zh, kz = _pinned_em(gp, a)
+                nbytes = n * k * 8
+                entry["e2e_mul"] = e2e_entry(
+                    lambda: gp.vec.mul_host(ah, bh, params, out=zh), steps, flush, stream, n,
+                    2 * nbytes, nbytes, "gfp_vec_mul_host, pinned element-major [2^22, 32]")
+                entry["e2e_mul"]["muls_per_s"] = entry["e2e_mul"].pop("elements_per_s")
+                del ah, bh, zh, ka, kb, kz
 
                 def step():
                     gp.fft_tensor(x, plan, out=y)
                 t = timed_loop(step, steps, 2, 1, flush, stream)
                 ms = sum(t) / len(t)
                 entry.update(ms_fwd=ms, fft_elements_per_s=N / (ms * 1e-3))
+                xh, keep = _pinned_em(gp, x)
+                entry["e2e_fft"] = e2e_entry(
+                    lambda: gp.fft_host(xh, plan, inplace=True), steps, flush, stream, N,
+                    N * k * 8, N * k * 8, "gfp_fft_exec_host, pinned element-major [2^18, 32]")
+                del xh, keep
             res[key] = entry
             del x, y
             torch.cuda.empty_cache()

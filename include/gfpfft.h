@@ -231,6 +231,23 @@ int gfp_fft_exec_exchange(const gfp_fft_plan *plan, const uint64_t *in, uint64_t
                           uint64_t *work, int64_t batch, int inverse, int in_canon, int out_canon,
                           uint64_t *const *dst, int world, int rank, void *stream);
 
+/* Device-side completion flags of the peer exchange (replacing host
+   barriers).  Each rank owns uint64 flags[slots][world] in device memory,
+   shared with the peers like the receive buffers; flags[slot][g] is written
+   only by rank g.  gfp_flag_signal stores `epoch` with system-scope release
+   semantics into peer_flags[g][slot][rank] for every rank g (after the
+   kernels queued before it on `stream`, whose stores it publishes);
+   gfp_flag_wait spins with system-scope acquire loads until every
+   my_flags[slot][g] >= epoch, so kernels queued after it see the peers'
+   published stores.  A wait not satisfied within max_spins polls writes
+   1 + slot * 256 + g into *err (device int) and returns -- a protocol error
+   is reported, never a hung GPU.  Both are one tiny stream-ordered kernel;
+   the host never blocks.  GFP_EINVAL for world > 16 or bad arguments. */
+int gfp_flag_signal(uint64_t *const *peer_flags, int world, int slot, int rank, uint64_t epoch,
+                    void *stream);
+int gfp_flag_wait(const uint64_t *my_flags, int world, int slot, uint64_t epoch,
+                  int64_t max_spins, int *err, void *stream);
+
 /* CUDA IPC for the exchange's peer pointers (one process per GPU):
    gfp_ipc_get_handle writes the 64-byte handle of the allocation holding ptr
    and ptr's byte offset in it; gfp_ipc_open maps a peer's handle and returns

@@ -78,6 +78,8 @@ SIGNATURES = {
                                       _int, _i64, _vp]),
     "gfp_fft_exec_exchange": (_int, [_vp, _u64p, _u64p, _u64p, _i64, _int, _int, _int,
                                      ctypes.POINTER(ctypes.c_uint64), _int, _int, _vp]),
+    "gfp_flag_signal": (_int, [ctypes.POINTER(ctypes.c_uint64), _int, _int, _int, _u64, _vp]),
+    "gfp_flag_wait": (_int, [_u64p, _int, _int, _u64, _i64, _vp, _vp]),
     "gfp_ipc_get_handle": (_int, [_vp, ctypes.c_char_p, ctypes.POINTER(_i64)]),
     "gfp_ipc_open": (_int, [ctypes.c_char_p, _i64, ctypes.POINTER(_vp)]),
     "gfp_ipc_close": (_int, [_vp, _i64]),

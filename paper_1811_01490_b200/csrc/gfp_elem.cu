@@ -469,6 +469,35 @@ int transpose_batched(const u64 *src, u64 *dst, int64_t batch, int64_t n_em, int
     return cuda_status();
 }
 
+int host_pipe_begin(HostPipe &hp, cudaStream_t caller)
+{
+    if (cudaEventCreateWithFlags(&hp.ev, cudaEventDisableTiming) != cudaSuccess)
+        return GFP_ECUDA;
+    cudaEventRecord(hp.ev, caller);
+    for (int i = 0; i < 2; i++) {
+        if (cudaStreamCreateWithFlags(&hp.s[i], cudaStreamNonBlocking) != cudaSuccess)
+            return GFP_ECUDA;
+        cudaStreamWaitEvent(hp.s[i], hp.ev, 0);
+    }
+    return cuda_status();
+}
+
+int host_pipe_end(HostPipe &hp, cudaStream_t caller)
+{
+    for (int i = 0; i < 2; i++) {
+        if (!hp.s[i])
+            continue;
+        cudaEventRecord(hp.ev, hp.s[i]);
+        cudaStreamWaitEvent(caller, hp.ev, 0);
+        cudaStreamDestroy(hp.s[i]);  // released once its queued work completes
+        hp.s[i] = nullptr;
+    }
+    if (hp.ev)
+        cudaEventDestroy(hp.ev);
+    hp.ev = nullptr;
+    return cuda_status();
+}
+
 static int g_num_sms[64];  // per device id (0 = not queried yet)
 
 int num_sms()
@@ -676,27 +705,45 @@ int gfp_vec_mul_host(const uint64_t *x, const uint64_t *y, uint64_t *z, int64_t 
     if (n == 0)
         return GFP_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    const size_t words = (size_t)n * k;
+    // chunks of ~128 MiB per operand through the two-stream pipeline: the
+    // H2D of one chunk overlaps the kernels and D2H of the other
+    const int64_t chunk = HOST_CHUNK_WORDS / k < n ? HOST_CHUNK_WORDS / k : n;
+    const int64_t nchunks = (n + chunk - 1) / chunk;
+    const size_t cw = (size_t)chunk * k;
+    const int nst = nchunks > 1 ? 2 : 1;
     u64 *buf = nullptr;
-    if (cudaMallocAsync(&buf, 4 * words * sizeof(u64), st) != cudaSuccess) {
+    if (cudaMalloc(&buf, (size_t)nst * 4 * cw * sizeof(u64)) != cudaSuccess) {
         cudaGetLastError();
         return GFP_ENOMEM;
     }
-    u64 *hx = buf, *hy = buf + words, *dx = buf + 2 * words, *dy = buf + 3 * words;
-    cudaMemcpyAsync(hx, x, words * sizeof(u64), cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(hy, y, words * sizeof(u64), cudaMemcpyHostToDevice, st);
-    e = transpose_batched(hx, dx, 1, n, n, k, 1, st);
-    if (!e)
-        e = transpose_batched(hy, dy, 1, n, n, k, 1, st);
-    if (!e)
-        e = gfp_vec_mul(dx, dy, 1, dx, n, k, r, st);
-    if (!e)
-        e = transpose_batched(dx, hx, 1, n, n, k, 0, st);
-    if (!e)
-        cudaMemcpyAsync(z, hx, words * sizeof(u64), cudaMemcpyDeviceToHost, st);
-    cudaFreeAsync(buf, st);
-    if (!e && cudaStreamSynchronize(st) != cudaSuccess)
+    HostPipe hp;
+    if (nst > 1)
+        e = host_pipe_begin(hp, st);
+    for (int64_t c = 0; c < nchunks && !e; c++) {
+        cudaStream_t s = nst > 1 ? hp.s[c & 1] : st;
+        u64 *hx = buf + (size_t)(c & (nst - 1)) * 4 * cw, *hy = hx + cw, *dx = hy + cw,
+            *dy = dx + cw;
+        const int64_t i0 = c * chunk, m = n - i0 < chunk ? n - i0 : chunk;
+        const size_t bytes = (size_t)m * k * sizeof(u64);
+        cudaMemcpyAsync(hx, x + i0 * k, bytes, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(hy, y + i0 * k, bytes, cudaMemcpyHostToDevice, s);
+        e = transpose_batched(hx, dx, 1, m, m, k, 1, s);
+        if (!e)
+            e = transpose_batched(hy, dy, 1, m, m, k, 1, s);
+        if (!e)
+            e = gfp_vec_mul(dx, dy, 1, dx, m, k, r, s);
+        if (!e)
+            e = transpose_batched(dx, hx, 1, m, m, k, 0, s);
+        if (!e)
+            cudaMemcpyAsync(z + i0 * k, hx, bytes, cudaMemcpyDeviceToHost, s);
+    }
+    if (nst > 1) {
+        const int e2 = host_pipe_end(hp, st);
+        e = e ? e : e2;
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess && !e)
         e = GFP_ECUDA;
+    cudaFree(buf);
     return e ? e : cuda_status();
 }
 

@@ -174,3 +174,84 @@ extern "C" int gfp_ipc_close(void *ptr, int64_t offset)
     }
     return GFP_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Device-side completion flags for the peer exchange (no host barriers).
+// Every rank owns a flag array in its device memory, shared with the peers
+// through the same IPC mappings as the receive buffers; flags[slot][g] is
+// written only by rank g.  A signal is a system-scope release store of an
+// epoch into every peer's flags[slot][rank] issued AFTER the kernels whose
+// stores it publishes (stream order: those kernels happen-before it); a wait
+// spins with system-scope acquire loads until every flags[slot][g] >= epoch,
+// and the kernels queued after it (stream order) see everything the peers
+// published -- the release/acquire pair carries the peers' NVLink stores.
+// A wait that does not see its epoch within max_spins polls records the slot
+// and rank in err[0] and returns instead of hanging the GPU.
+
+__global__ void k_flag_signal(PeerPtrs flags, int world, int slot, int rank,
+                              unsigned long long epoch)
+{
+    const int g = threadIdx.x;
+    if (g >= world)
+        return;
+    unsigned long long *f = reinterpret_cast<unsigned long long *>(flags.p[0]);
+#pragma unroll 1
+    for (int q = 1; q < XMAX; q++)
+        if (q == g)
+            f = reinterpret_cast<unsigned long long *>(flags.p[q]);
+    f += (int64_t)slot * world + rank;
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(epoch) : "memory");
+}
+
+__global__ void k_flag_wait(const unsigned long long *flags, int world, int slot,
+                            unsigned long long epoch, long long max_spins, int *err)
+{
+    const int g = threadIdx.x;
+    if (g < world) {
+        const unsigned long long *f = flags + (int64_t)slot * world + g;
+        unsigned long long v = 0;
+        long long spins = 0;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+            if (v >= epoch)
+                break;
+            if (++spins > max_spins) {
+                atomicCAS(err, 0, 1 + slot * 256 + g);
+                break;
+            }
+            __nanosleep(64);
+        }
+    }
+    __syncthreads();
+}
+
+extern "C" int gfp_flag_signal(uint64_t *const *peer_flags, int world, int slot, int rank,
+                               uint64_t epoch, void *stream)
+{
+    if (!peer_flags || world < 1 || world > XMAX || rank < 0 || rank >= world || slot < 0 ||
+        slot > 255)
+        return GFP_EINVAL;
+    PeerPtrs pp;
+    memset(&pp, 0, sizeof(pp));
+    for (int g = 0; g < world; g++) {
+        if (!peer_flags[g])
+            return GFP_EINVAL;
+        pp.p[g] = peer_flags[g];
+    }
+    k_flag_signal<<<1, 32, 0, (cudaStream_t)stream>>>(pp, world, slot, rank,
+                                                      (unsigned long long)epoch);
+    return cuda_status();
+}
+
+extern "C" int gfp_flag_wait(const uint64_t *my_flags, int world, int slot, uint64_t epoch,
+                             int64_t max_spins, int *err, void *stream)
+{
+    if (!my_flags || !err || world < 1 || world > XMAX || slot < 0 || slot > 255 ||
+        max_spins < 1)
+        return GFP_EINVAL;
+    k_flag_wait<<<1, 32, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const unsigned long long *>(my_flags), world, slot,
+        (unsigned long long)epoch, (long long)max_spins, err);
+    return cuda_status();
+}

@@ -19,6 +19,20 @@ int num_sms();
 dim3 grid_for(int64_t work, int threads);
 int cuda_status();
 int check_kr(int k, u64 r);
+// Two-stream pipeline of the host entry points: chunk i of a large call runs
+// on stream s[i % 2] (its copies and kernels in order), so one chunk's H2D
+// overlaps the other's kernels and D2H (PCIe is full duplex).  begin makes
+// both streams wait for the caller's stream; end makes the caller's stream
+// wait for both and releases them.
+struct HostPipe {
+    cudaStream_t s[2] = {nullptr, nullptr};
+    cudaEvent_t ev = nullptr;
+};
+int host_pipe_begin(HostPipe &hp, cudaStream_t caller);
+int host_pipe_end(HostPipe &hp, cudaStream_t caller);
+// words of one pipeline chunk (128 MiB)
+constexpr int64_t HOST_CHUNK_WORDS = (int64_t)1 << 24;
+
 // element-major [B][n_em][k] <-> digit-major [B][k][n_dm] (to_dm: zero-pad
 // i >= n_em; else write i < n_em only), tiled through shared memory
 int transpose_batched(const u64 *src, u64 *dst, int64_t batch, int64_t n_em, int64_t n_dm, int k,

@@ -713,51 +713,89 @@ int gfp_poly_mul_host(gfp_fft_plan *p, const uint64_t *f, const uint64_t *g, uin
     return gfp_poly_mul_host2(p, f, p->N, g, p->N, out, batch, stream);
 }
 
+// one chunk of gfp_fft_exec_host: transforms [b0, b0 + nb) of the host
+// array v (element-major), on stream s with device buffers a / b / w (+ stg
+// for pageable input), nb k N words each
+static int exec_host_chunk(gfp_fft_plan *p, uint64_t *v, u64 *mv, int64_t b0, int64_t nb,
+                           int inverse, u64 *a, u64 *b, u64 *w, u64 *stg, cudaStream_t s)
+{
+    const int k = p->k;
+    const int64_t N = p->N, ew = (int64_t)k * N, vw = ew * nb;
+    const u64 *src;
+    if (mv) {
+        src = mv + b0 * ew;
+    } else {
+        cudaMemcpyAsync(stg, v + b0 * ew, sizeof(u64) * vw, cudaMemcpyHostToDevice, s);
+        src = stg;
+    }
+    int err;
+    if (!em_io_supported(p)) {
+        // no element-major kernel for this k: one batched transpose on each
+        // side of the transform
+        err = transpose_batched(src, b, nb, N, N, k, 1, s);
+        if (!err)
+            err = run_transform(p, b, b, w, nullptr, nb, inverse ? 1 : 0, 1, 1, s);
+        if (!err)
+            err = transpose_batched(b, a, nb, N, N, k, 0, s);
+        if (err)
+            return err;
+        p->last_launches += 2;
+        cudaMemcpyAsync(v + b0 * ew, a, sizeof(u64) * vw, cudaMemcpyDeviceToHost, s);
+        return GFP_OK;
+    }
+    // a single-pass transform would read and write v in the same launch:
+    // stage its output
+    const bool stage_out = !mv || p->e == 1;
+    PassIO em = {src, nullptr, N, 0, stage_out ? a : mv + b0 * ew, N, nullptr, 0, 0};
+    err = run_transform(p, b, b, w, nullptr, nb, inverse ? 1 : 0, 1, 1, s, &em);
+    if (err)
+        return err;
+    if (stage_out)
+        cudaMemcpyAsync(v + b0 * ew, a, sizeof(u64) * vw, cudaMemcpyDeviceToHost, s);
+    return GFP_OK;
+}
+
 int gfp_fft_exec_host(gfp_fft_plan *p, uint64_t *v, int64_t batch, int inverse, void *stream)
 {
     if (!p || !v || batch < 1)
         return GFP_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     const int k = p->k;
-    const int64_t N = p->N, vw = (int64_t)k * N * batch;
+    const int64_t N = p->N, ew = (int64_t)k * N;
     begin_call(p);
     u64 *mv = em_io_supported(p) ? mapped_alias(v) : nullptr;
-    // a single-pass transform would read and write v in the same launch:
-    // stage its output
-    const bool stage_out = !mv || p->e == 1;
-    int err = ensure_host_scratch(p, 3 * vw + (mv ? 0 : vw));
+    // batches of more than ~128 MiB go through the two-stream pipeline in
+    // chunks of transforms: one chunk's host traffic overlaps the other's
+    // kernels (and H2D overlaps D2H)
+    int64_t per = HOST_CHUNK_WORDS / ew;
+    if (per < 1)
+        per = 1;
+    if (per > batch)
+        per = batch;
+    if (per > GFP_MAX_GRID_Y)
+        per = GFP_MAX_GRID_Y;
+    const int64_t nchunks = (batch + per - 1) / per;
+    const int nst = nchunks > 1 ? 2 : 1;
+    const int64_t cw = ew * per;  // words of one chunk buffer
+    int err = ensure_host_scratch(p, (int64_t)nst * 4 * cw);
     if (err)
         return err;
-    u64 *a = p->h_dev, *b = a + vw, *w = b + vw;
-    const u64 *src = mv;
-    if (!mv) {
-        u64 *stg = w + vw;
-        cudaMemcpyAsync(stg, v, sizeof(u64) * vw, cudaMemcpyHostToDevice, st);
-        src = stg;
+    HostPipe hp;
+    if (nst > 1)
+        err = host_pipe_begin(hp, st);
+    for (int64_t c = 0; c < nchunks && !err; c++) {
+        cudaStream_t s = nst > 1 ? hp.s[c & 1] : st;
+        u64 *a = p->h_dev + (c & (nst - 1)) * 4 * cw, *b = a + cw, *w = b + cw, *stg = w + cw;
+        const int64_t b0 = c * per, nb = batch - b0 < per ? batch - b0 : per;
+        err = exec_host_chunk(p, v, mv, b0, nb, inverse, a, b, w, stg, s);
     }
-    if (!em_io_supported(p)) {
-        // no element-major kernel for this k: one batched transpose on each
-        // side of the transform
-        err = transpose_batched(src, b, batch, N, N, k, 1, st);
-        if (!err)
-            err = run_transform(p, b, b, w, nullptr, batch, inverse ? 1 : 0, 1, 1, st);
-        if (!err)
-            err = transpose_batched(b, a, batch, N, N, k, 0, st);
-        if (err)
-            return err;
-        p->last_launches += 2;
-        cudaMemcpyAsync(v, a, sizeof(u64) * vw, cudaMemcpyDeviceToHost, st);
-    } else {
-        PassIO em = {src, nullptr, N, 0, stage_out ? a : mv, N, nullptr, 0, 0};
-        err = run_transform(p, b, b, w, nullptr, batch, inverse ? 1 : 0, 1, 1, st, &em);
-        if (err)
-            return err;
-        if (stage_out)
-            cudaMemcpyAsync(v, a, sizeof(u64) * vw, cudaMemcpyDeviceToHost, st);
+    if (nst > 1) {
+        const int e2 = host_pipe_end(hp, st);
+        err = err ? err : e2;
     }
-    if (cudaStreamSynchronize(st) != cudaSuccess)
-        return GFP_ECUDA;
-    return cuda_status();
+    if (cudaStreamSynchronize(st) != cudaSuccess && !err)
+        err = GFP_ECUDA;
+    return err ? err : cuda_status();
 }
 
 }  // extern "C"

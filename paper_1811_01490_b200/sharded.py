@@ -48,6 +48,7 @@ class ShardedFFT:
         self.c1 = N1 // world  # local rows
         self.c2 = N2 // world  # local columns
         self.peer = None       # PeerExchange: the transpose as peer stores
+        self.exchange_path = "all_to_all_single" if world > 1 else "local"
 
     def exchange_shapes(self):
         return {"rows": (self.c1, self.k, self.N2), "cols": (self.c2, self.k, self.N1)}
@@ -58,9 +59,18 @@ class ShardedFFT:
         the last pass of the preceding DFTs (gfp_fft_exec_exchange) when
         `fuse` and the pass kernel supports it, else one
         gfp_exchange_transpose kernel (instead of pack / all-to-all / unpack)."""
-        self.peer = PeerExchange(self.exchange_shapes(), self.rank, self.world, self.group,
-                                 device, local_peers)
+        try:
+            self.peer = PeerExchange(self.exchange_shapes(), self.rank, self.world, self.group,
+                                     device, local_peers)
+        except PeerIPCError as exc:
+            # every rank saw the same failure (PeerExchange agrees on it), so
+            # every rank stays on the NCCL all-to-all path
+            self.peer = None
+            self.exchange_path = "all_to_all_single (peer IPC unavailable: %s)" % str(exc)[:200]
+            return self
         self.peer.fuse = fuse
+        self.exchange_path = "peer stores (%s)" % ("fused into the last pass" if fuse
+                                                   else "gfp_exchange_transpose")
         return self
 
     # -- exchange ---------------------------------------------------------
@@ -88,20 +98,24 @@ class ShardedFFT:
                                    out_canon=True, ft_row0=self.rank * self.c1)
         return self.ops.fft(_u64(rows), "N2", inverse=False)
 
-    def columns_to_rows(self, cols):
+    def columns_to_rows(self, cols, wait=True):
         """Steps 1-3: column DFTs, twiddle and the transpose; returns this
-        rank's rows [N1/G, k, N2] (before the row DFTs)."""
+        rank's rows [N1/G, k, N2] (before the row DFTs).  wait=False (peer
+        exchange, emulated ranks): return after publishing this rank's
+        stores; peer.finish("rows") completes the exchange."""
         G, k, c1, c2 = self.world, self.k, self.c1, self.c2
         if self.peer is not None:
             if self.peer.fuse and getattr(self.ops, "fused", False):
                 # the column DFTs' last pass stores straight into the owners'
                 # row buffers (gfp_fft_exec_exchange)
-                if self.peer.bracket(lambda: self.ops.fft_exchange(
-                        cols, "N1", False, True, False, self.peer.addrs["rows"],
-                        G, self.rank)):
+                res = self.peer.begin("rows", lambda: self.ops.fft_exchange(
+                    cols, "N1", False, True, False, self.peer.addrs["rows"], G, self.rank))
+                if res:
+                    if wait:
+                        self.peer.finish("rows", res)
                     return self.peer.recv["rows"]
             y = self.forward_columns(cols)  # one kernel stores into every rank's buffer
-            return self.peer.transpose("rows", y, A=c2, B=self.N1)
+            return self.peer.transpose("rows", y, A=c2, B=self.N1, wait=wait)
         y = self.forward_columns(cols)
         send = _i64(y).view(c2, k, G, c1).permute(2, 0, 1, 3).contiguous()
         recv = self._all_to_all(send)                                  # [g, n2l, d, k1l]
@@ -109,7 +123,10 @@ class ShardedFFT:
 
     def forward(self, cols):
         """cols [N2/G, k, N1] (canonical) -> rows [N1/G, k, N2] (canonical)."""
-        return self.forward_rows(self.columns_to_rows(cols))
+        out = self.forward_rows(self.columns_to_rows(cols))
+        if self.peer is not None:
+            self.peer.consumed("rows")  # the row DFTs have read the receive buffer
+        return out
 
     # -- inverse ----------------------------------------------------------
     def inverse_rows(self, rows):
@@ -126,18 +143,20 @@ class ShardedFFT:
         cols = self.ops.twiddle(_u64(cols), self.rank * self.c2, inverse=True)
         return self.ops.fft(cols, "N1", inverse=True)
 
-    def rows_to_columns(self, rows):
+    def rows_to_columns(self, rows, wait=True):
         """Inverse row DFTs and the transpose back; returns this rank's
         columns [N2/G, k, N1] (before the conjugate twiddle)."""
         G, k, c1, c2 = self.world, self.k, self.c1, self.c2
         if self.peer is not None:
             if self.peer.fuse and getattr(self.ops, "fused", False):
-                if self.peer.bracket(lambda: self.ops.fft_exchange(
-                        rows, "N2", True, True, False, self.peer.addrs["cols"],
-                        G, self.rank)):
+                res = self.peer.begin("cols", lambda: self.ops.fft_exchange(
+                    rows, "N2", True, True, False, self.peer.addrs["cols"], G, self.rank))
+                if res:
+                    if wait:
+                        self.peer.finish("cols", res)
                     return self.peer.recv["cols"]
             z = self.inverse_rows(rows)
-            return self.peer.transpose("cols", z, A=c1, B=self.N2)
+            return self.peer.transpose("cols", z, A=c1, B=self.N2, wait=wait)
         z = self.inverse_rows(rows)
         send = _i64(z).view(c1, k, G, c2).permute(2, 0, 1, 3).contiguous()
         recv = self._all_to_all(send)                                  # [g, k1l, d, n2l]
@@ -145,7 +164,10 @@ class ShardedFFT:
 
     def inverse(self, rows):
         """rows [N1/G, k, N2] -> cols [N2/G, k, N1]; inverse of forward()."""
-        return self.inverse_columns(self.rows_to_columns(rows))
+        out = self.inverse_columns(self.rows_to_columns(rows))
+        if self.peer is not None:
+            self.peer.consumed("cols")
+        return out
 
     # -- global <-> local layouts (tests and benchmark data placement) ----
     def scatter_columns(self, x):
@@ -168,18 +190,39 @@ def _barrier(group):
     dist.barrier(group=group)
 
 
+class PeerIPCError(RuntimeError):
+    """CUDA IPC / peer access unavailable on some rank."""
+
+
 class PeerExchange:
     """Receive buffers of the four-step transpose and every rank's address of
     them: CUDA IPC handles (gfp_ipc_get_handle / gfp_ipc_open) gathered once
-    with all_gather_object, so each exchange is one gfp_exchange_transpose
-    launch writing over NVLink into the owners' buffers.  Two host barriers
-    bracket it: peers have finished reading their buffers (previous call)
-    before the stores start, and every store into this rank's buffer has
-    landed before it is read.
+    with all_gather_object, so each exchange is one kernel writing over NVLink
+    into the owners' buffers (the fused XCH pass or gfp_exchange_transpose).
+
+    Synchronisation of an exchange named n ("rows" / "cols"), three modes:
+      host   (default) two host barriers: peers finished reading their
+             buffers (previous exchange) before the stores start, and every
+             store into this rank's buffer landed before it is read;
+      nccl   the same two barriers as stream-ordered one-element NCCL
+             all-reduces (use_device_barrier);
+      flags  device-side completion flags, no host involvement
+             (use_device_flags): per exchange an epoch e,
+               wait  consumed[n][g] >= e - 1   (peer g read its previous buffer)
+               the stores (fn)
+               signal ready[n] = e into every peer   (st.release.sys)
+               wait  ready[n][g] >= e            (every peer's stores landed)
+             and after the kernel that reads recv[n], consumed(n) signals
+             consumed[n] = e (gfp_flag_signal / gfp_flag_wait).
+    begin(n, fn) / finish(n) split an exchange at the point where a rank
+    waits for its peers (the emulated-ranks tests issue every rank's begin
+    before any finish on one stream); bracket(fn, n) is both.
 
     ``local_peers`` (tests, one process): a list of G PeerExchange-like
     receive-buffer dicts on this device standing in for the peers (no
     barriers; the caller runs the ranks' stages in order)."""
+
+    SLOTS = {"rows": (0, 2), "cols": (1, 3)}  # (ready, consumed) flag slots
 
     def __init__(self, shapes, rank, world, group=None, device=None, local_peers=None):
         import ctypes
@@ -188,61 +231,107 @@ class PeerExchange:
         self._opened = []
         self.addrs = {}
         self.fuse = True
-        self.device_barrier = False  # opt-in: use_device_barrier()
+        self.mode = "host"
+        self.device_barrier = False
         self._flag = None
+        self.max_spins = 1 << 24  # ~1 s of polling per wait before an error is recorded
+        self.epoch = {n: 0 for n in self.SLOTS}
         self.local = local_peers is not None
         if self.local:
-            self.recv = local_peers[rank]
+            mine = local_peers[rank]
+            self.recv = {n: t for n, t in mine.items() if not n.startswith("__")}
+            self.flags, self.err = mine["__flags"], mine["__err"]
             for n in shapes:
                 self.addrs[n] = [p[n].data_ptr() for p in local_peers]
+            self.flag_addrs = [p["__flags"].data_ptr() for p in local_peers]
             return
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.recv = {n: torch.empty(sh, dtype=torch.int64, device=dev).view(torch.uint64)
                      for n, sh in shapes.items()}
+        self.flags = torch.zeros((4, world), dtype=torch.int64, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
         if world == 1:
             self.addrs = {n: [t.data_ptr()] for n, t in self.recv.items()}
+            self.flag_addrs = [self.flags.data_ptr()]
             return
         import torch.distributed as dist
         lib = _lib.load()
-        mine = {}
-        for n, t in self.recv.items():
-            h = ctypes.create_string_buffer(64)
-            off = ctypes.c_int64(0)
-            _lib.check(lib.gfp_ipc_get_handle(ctypes.c_void_p(t.data_ptr()), h,
-                                              ctypes.byref(off)), "gfp_ipc_get_handle")
-            mine[n] = (h.raw, off.value)
+        shared = dict(self.recv, __flags=self.flags)
+        mine, failure = {}, None
+        try:
+            for n, t in shared.items():
+                h = ctypes.create_string_buffer(64)
+                off = ctypes.c_int64(0)
+                _lib.check(lib.gfp_ipc_get_handle(ctypes.c_void_p(t.data_ptr()), h,
+                                                  ctypes.byref(off)), "gfp_ipc_get_handle")
+                mine[n] = (h.raw, off.value)
+        except Exception as exc:  # reported to every rank below
+            failure = "rank %d: %s" % (rank, exc)
         every = [None] * world
-        dist.all_gather_object(every, mine, group=group)
-        for n, t in self.recv.items():
-            addrs = []
-            for g in range(world):
-                if g == rank:
-                    addrs.append(t.data_ptr())
-                    continue
-                raw, off = every[g][n]
-                ptr = ctypes.c_void_p(0)
-                _lib.check(lib.gfp_ipc_open(raw, off, ctypes.byref(ptr)), "gfp_ipc_open")
-                addrs.append(ptr.value)
-                self._opened.append((ptr.value, off))
-            self.addrs[n] = addrs
+        dist.all_gather_object(every, (mine, failure), group=group)
+        addrs = {n: [] for n in shared}
+        try:
+            bad = [f for _, f in every if f]
+            if bad:
+                raise PeerIPCError("; ".join(bad))
+            for n, t in shared.items():
+                for g in range(world):
+                    if g == rank:
+                        addrs[n].append(t.data_ptr())
+                        continue
+                    raw, off = every[g][0][n]
+                    ptr = ctypes.c_void_p(0)
+                    _lib.check(lib.gfp_ipc_open(raw, off, ctypes.byref(ptr)), "gfp_ipc_open")
+                    addrs[n].append(ptr.value)
+                    self._opened.append((ptr.value, off))
+            failure = None
+        except Exception as exc:
+            failure = "rank %d: %s" % (rank, exc)
+        # every rank agrees on the outcome before anyone uses a peer pointer
+        outcome = [None] * world
+        dist.all_gather_object(outcome, failure, group=group)
+        bad = [f for f in outcome if f]
+        if bad:
+            self.close()
+            raise PeerIPCError("; ".join(bad))
+        self.flag_addrs = addrs.pop("__flags")
+        self.addrs = addrs
 
     def use_device_barrier(self):
         """Replace the two host barriers by stream-ordered NCCL barriers (only
-        with an NCCL group; a no-op otherwise)."""
+        with an NCCL group -- 'nccl' or a device-specific 'cuda:nccl' backend;
+        a no-op otherwise)."""
         if self.world > 1 and not self.local:
             import torch.distributed as dist
-            if dist.get_backend(self.group) == "nccl":
+            if "nccl" in str(dist.get_backend(self.group)):
+                self.mode = "nccl"
                 self.device_barrier = True
                 self._flag = torch.zeros(1, dtype=torch.int32,
                                          device=next(iter(self.recv.values())).device)
         return self
 
+    def use_device_flags(self, max_spins=None):
+        """Device-side completion flags instead of barriers (see the class
+        docstring): the host never blocks between the exchange's kernels."""
+        self.mode = "flags"
+        if max_spins is not None:
+            self.max_spins = int(max_spins)
+        return self
+
     @staticmethod
     def local_buffers(shapes, world, device="cuda"):
-        """Receive buffers of `world` emulated ranks on one device."""
-        return [{n: torch.empty(sh, dtype=torch.int64, device=device).view(torch.uint64)
-                 for n, sh in shapes.items()} for _ in range(world)]
+        """Receive buffers (and flag arrays) of `world` emulated ranks on one
+        device."""
+        out = []
+        for _ in range(world):
+            d = {n: torch.empty(sh, dtype=torch.int64, device=device).view(torch.uint64)
+                 for n, sh in shapes.items()}
+            d["__flags"] = torch.zeros((4, world), dtype=torch.int64, device=device)
+            d["__err"] = torch.zeros(1, dtype=torch.int32, device=device)
+            out.append(d)
+        return out
 
+    # -- the three synchronisation modes ------------------------------------
     def _sync(self):
         if self.device_barrier:
             # stream-ordered barrier: a one-element NCCL all-reduce on the
@@ -253,19 +342,78 @@ class PeerExchange:
         else:
             _barrier(self.group)
 
-    def bracket(self, fn):
-        """Run fn (stores into the peers' buffers) between the two barriers;
-        returns fn's result.  Every rank takes the same branch (the
-        supported-or-not outcome of fn depends only on shapes)."""
-        many = self.world > 1 and not self.local
-        if many:
+    def _stream(self):
+        import ctypes
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def _signal(self, slot, epoch):
+        import ctypes
+        from . import _lib
+        ptrs = (ctypes.c_uint64 * self.world)(*self.flag_addrs)
+        _lib.check(_lib.load().gfp_flag_signal(ptrs, self.world, slot, self.rank, epoch,
+                                               self._stream()), "gfp_flag_signal")
+
+    def _wait(self, slot, epoch):
+        import ctypes
+        from . import _lib
+        _lib.check(_lib.load().gfp_flag_wait(
+            ctypes.c_void_p(self.flags.data_ptr()), self.world, slot, epoch, self.max_spins,
+            ctypes.c_void_p(self.err.data_ptr()), self._stream()), "gfp_flag_wait")
+
+    def _flags_on(self):
+        return self.mode == "flags" and (self.world > 1 or self.local)
+
+    def begin(self, name, fn):
+        """The first half of an exchange: wait until the peers may be written
+        (flags: their previous buffers consumed; barrier modes: a barrier),
+        run fn (the stores into every rank's recv[name]; False = this route
+        is unsupported and nothing was stored) and publish the stores."""
+        if self._flags_on():
+            ready, consumed = self.SLOTS[name]
+            epoch = self.epoch[name] + 1
+            self._wait(consumed, epoch - 1)
+            res = fn()
+            if res is not False:
+                self._signal(ready, epoch)
+                self.epoch[name] = epoch
+            return res
+        if self.world > 1 and not self.local:
             self._sync()
-        res = fn()
-        if many and res is not False:
+        return fn()
+
+    def finish(self, name, res=True):
+        """The second half: every peer's stores into recv[name] have landed."""
+        if res is False:
+            return
+        if self._flags_on():
+            self._wait(self.SLOTS[name][0], self.epoch[name])
+        elif self.world > 1 and not self.local:
             self._sync()
+
+    def bracket(self, fn, name="rows"):
+        """begin + finish: run fn (stores into the peers' buffers) between the
+        two synchronisation points; returns fn's result.  Every rank takes
+        the same branch (the supported-or-not outcome of fn depends only on
+        shapes)."""
+        res = self.begin(name, fn)
+        self.finish(name, res)
         return res
 
-    def transpose(self, name, src, A, B):
+    def consumed(self, name):
+        """After the kernel that read recv[name] (flags mode): tell every peer
+        it may write the buffer again."""
+        if self._flags_on():
+            self._signal(self.SLOTS[name][1], self.epoch[name])
+
+    def check(self):
+        """Raise if a flag wait timed out (reads the device error word)."""
+        e = int(self.err.item())
+        if e:
+            e -= 1
+            raise RuntimeError("peer-exchange flag wait timed out: slot %d, rank %d"
+                               % (e // 256, e % 256))
+
+    def transpose(self, name, src, A, B, wait=True):
         """src [A, k, B] -> every rank's recv[name] (see gfp_exchange_transpose);
         returns this rank's receive buffer."""
         import ctypes
@@ -279,7 +427,9 @@ class PeerExchange:
                 ctypes.c_void_p(src.data_ptr()), ptrs, self.world, self.rank, A, k, B,
                 ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
                 "gfp_exchange_transpose")
-        self.bracket(run)
+        res = self.begin(name, run)
+        if wait:
+            self.finish(name, res)
         return self.recv[name]
 
     def close(self):

@@ -92,15 +92,22 @@ def mul(x, y, params):
     return z
 
 
-def mul_host(x, y, params):
+def mul_host(x, y, params, out=None):
     """Element-wise product of element-major host arrays [n, k] (uint64) ->
-    new [n, k] array (gfp_vec_mul_host: the whole H2D / multiply / D2H)."""
+    [n, k] array (gfp_vec_mul_host: the whole H2D / multiply / D2H); `out`
+    (e.g. a pinned buffer) receives the product when given."""
     import ctypes as C
     x = np.ascontiguousarray(np.asarray(x, dtype=np.uint64))
     y = np.ascontiguousarray(np.asarray(y, dtype=np.uint64))
     if x.shape != y.shape or x.ndim != 2 or x.shape[1] != params.k:
         raise ValueError("operands must be [n, k] arrays of the same shape")
-    z = np.empty_like(x)
+    if out is None:
+        z = np.empty_like(x)
+    else:
+        z = out
+        if not (isinstance(z, np.ndarray) and z.dtype == np.uint64 and z.shape == x.shape
+                and z.flags.c_contiguous):
+            raise ValueError("out must be a C-contiguous uint64 array shaped like x")
     _lib.check(_lib.load().gfp_vec_mul_host(C.c_void_p(x.ctypes.data), C.c_void_p(y.ctypes.data),
                                            C.c_void_p(z.ctypes.data), x.shape[0], params.k,
                                            params.r, _stream()), "gfp_vec_mul_host")

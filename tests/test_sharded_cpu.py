@@ -162,15 +162,19 @@ class GlooPeer:
         self.recv = {n: torch.empty(sh, dtype=torch.int64) for n, sh in shapes.items()}
         self.barriers = 0
 
-    def bracket(self, fn):
+    def begin(self, name, fn):
         dist.barrier()
-        res = fn()
+        return fn()
+
+    def finish(self, name, res=True):
         if res is not False:
             dist.barrier()
         self.barriers += 1
-        return res
 
-    def transpose(self, name, src, A, B):
+    def consumed(self, name):
+        pass
+
+    def _store(self, name, src, A, B):
         G, b = self.world, B // self.world
         s = src.view(torch.int64) if src.dtype != torch.int64 else src
         kk = s.shape[1]
@@ -180,8 +184,55 @@ class GlooPeer:
             got = torch.empty_like(send)
             dist.all_to_all_single(got, send)                             # [src rank][a][d][bl]
             self.recv[name].view(b, kk, G, A)[:] = got.permute(3, 2, 0, 1)
-        self.bracket(run)
+        return run
+
+    def transpose(self, name, src, A, B, wait=True):
+        res = self.begin(name, self._store(name, src, A, B))
+        if wait:
+            self.finish(name, res)
         return self.recv[name]
+
+
+def _flag_peer_class():
+    from paper_1811_01490_b200.sharded import PeerExchange
+
+    class CpuFlagPeer(PeerExchange):
+        """sharded.PeerExchange in device-flag mode with the two flag
+        kernels replaced by their host equivalents on flag arrays in shared
+        CPU memory (one per rank, written by the peers): the protocol code
+        itself -- begin / finish / consumed, epochs, slots -- is the
+        product's, run by two real processes."""
+
+        def __init__(self, shapes, rank, world, shared_flags, log):
+            self.rank, self.world, self.group = rank, world, None
+            self.fuse, self.local, self.mode = True, False, "flags"
+            self.device_barrier = False
+            self.epoch = {n: 0 for n in self.SLOTS}
+            self.recv = {n: torch.empty(sh, dtype=torch.int64) for n, sh in shapes.items()}
+            self.shared, self.log, self.barriers = shared_flags, log, 0
+            self._opened = []
+
+        def _signal(self, slot, epoch):  # gfp_flag_signal
+            for g in range(self.world):
+                self.shared[g][slot, self.rank] = epoch
+            self.log.append(("signal", slot, epoch))
+
+        def _wait(self, slot, epoch):    # gfp_flag_wait (bounded spin)
+            import time
+            t_end = time.monotonic() + 60
+            while not bool((self.shared[self.rank][slot] >= epoch).all()):
+                if time.monotonic() > t_end:
+                    raise RuntimeError("flag wait timed out: slot %d epoch %d" % (slot, epoch))
+                time.sleep(0.001)
+            self.log.append(("wait", slot, epoch))
+
+        def transpose(self, name, src, A, B, wait=True):
+            res = self.begin(name, GlooPeer._store(self, name, src, A, B))
+            if wait:
+                self.finish(name, res)
+            return self.recv[name]
+
+    return CpuFlagPeer
 
 
 def _peer_worker(rank, world, port, N1, N2, q):
@@ -207,6 +258,61 @@ def _peer_worker(rank, world, port, N1, N2, q):
         q.put((rank, bool(ok_fwd), bool(ok_inv), sh.peer.barriers))
     finally:
         dist.destroy_process_group()
+
+
+def _flag_worker(rank, world, port, N1, N2, flags, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1811_01490_b200.sharded import ShardedFFT
+        N = N1 * N2
+        _, omega = O.gfp_root(k, R8, N)
+        ops = OracleShardOps(N1, N2, omega)
+        sh = ShardedFFT(ops, k, N1, N2, rank, world)
+        log = []
+        sh.peer = _flag_peer_class()(sh.exchange_shapes(), rank, world, flags, log)
+        x = O.random_elements(6, k, R8, N)
+        xd = torch.from_numpy(np.ascontiguousarray(x.T).view(np.int64))
+        cols = sh.scatter_columns(xd)
+        want = ops.big.forward(x)
+        idx = sh.gather_rows_index().numpy()
+        ok = []
+        for _ in range(3):  # three round trips: epochs 1..3 on both exchanges
+            rows = sh.forward(cols)
+            ok.append(np.array_equal(_np(rows).transpose(0, 2, 1).reshape(-1, k),
+                                     want[idx.reshape(-1)]))
+            ok.append(np.array_equal(_np(sh.inverse(rows)), _np(cols)))
+        q.put((rank, all(ok), dict(sh.peer.epoch), log))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_peer_exchange_device_flag_protocol_gloo():
+    # the device-flag synchronisation of PeerExchange (begin / finish /
+    # consumed with epochs) driving ShardedFFT's peer-exchange branches in two
+    # real processes, the flag kernels emulated on shared CPU memory
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    flags = [torch.zeros((4, 2), dtype=torch.int64).share_memory_() for _ in range(2)]
+    procs = [ctx.Process(target=_flag_worker, args=(r, 2, port, 16, 256, flags, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    res = sorted((q.get(timeout=5) for _ in range(2)), key=lambda t: t[0])
+    assert all(p.exitcode == 0 for p in procs)
+    for rank, ok, epoch, log in res:
+        assert ok and epoch == {"rows": 3, "cols": 3}
+        # per exchange: wait(consumed, e-1), signal(ready, e), wait(ready, e),
+        # then signal(consumed, e) after the reading DFTs
+        assert log[:4] == [("wait", 2, 0), ("signal", 0, 1), ("wait", 0, 1), ("signal", 2, 1)]
+        assert log[4:8] == [("wait", 3, 0), ("signal", 1, 1), ("wait", 1, 1), ("signal", 3, 1)]
+        assert ("wait", 2, 2) in log and ("signal", 3, 3) in log
+    # every flag ends at the last epoch
+    assert all(int(f.min()) == 3 for f in flags)
 
 
 def test_sharded_peer_exchange_two_ranks_gloo():
