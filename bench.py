@@ -705,6 +705,30 @@ def multi_gpu_configs(args, ws, rank, dev, flush, stream):
                         "scaling": "strong"}
             except Exception as exc:
                 res["c4_sharded_peer_devsync"] = {"error": str(exc)[:300]}
+            try:
+                # device-side completion flags (release / acquire epochs
+                # between the ranks' kernels) instead of any barrier -- one
+                # GPU per rank only (NCCL), never ranks sharing a device
+                import torch.distributed as dist
+                if shp.peer is not None and "nccl" in str(dist.get_backend()):
+                    shp.peer.use_device_flags()
+                    t = timed_loop(lambda: shp.forward(cols), steps, 2, ws, flush, stream)
+                    ms = max_over_ranks(sum(t) / len(t), ws)
+                    rows = shp.forward(cols)
+                    okf = bool((shp.inverse(rows).view(torch.int64)
+                                == cols.view(torch.int64)).all().item())
+                    samef = bool((rows.view(torch.int64)
+                                  == sh.forward(cols).view(torch.int64)).all().item())
+                    shp.peer.check()
+                    res["c4_sharded_peer_flags"] = {
+                        "workload": "C4 fwd k=8 N=2^24 four-step, peer-store exchange, "
+                                    "device completion flags",
+                        "n_gpus": ws, "ms_fwd": ms, "elements_per_s": N / (ms * 1e-3),
+                        "roundtrip_exact": okf, "equals_all_to_all_path": samef,
+                        "scaling": "strong"}
+            except Exception as exc:
+                res["c4_sharded_peer_flags"] = {"error": str(exc)[:300]}
+        res["c4_sharded_peer"]["exchange_path"] = shp.exchange_path
         if shp.peer is not None:
             shp.peer.close()
         del cols, rows
@@ -712,7 +736,60 @@ def multi_gpu_configs(args, ws, rank, dev, flush, stream):
     except Exception as exc:
         res.setdefault("c4_sharded", {"error": str(exc)[:300]})
         res["c4_sharded_peer"] = {"error": str(exc)[:300]}
+    if ws > 1:
+        res["scaling"] = scaling_block(args, ws, rank, res, flush, stream)
     return res
+
+
+def scaling_block(args, ws, rank, res, flush, stream):
+    """At N > 1: the same configs on rank 0's GPU alone in this run (the N = 1
+    baseline of the sharded numbers above), their ratio, and the
+    communicator that carried the exchange (checkable rank count)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1811_01490_b200 as gp
+    out = {"world_size": dist.get_world_size(), "backend": str(dist.get_backend()),
+           "nccl_version": ".".join(str(v) for v in torch.cuda.nccl.version())
+           if hasattr(torch.cuda, "nccl") else None}
+    one = {}
+    if rank == 0:
+        steps = max(3, min(args.steps, 10))
+        try:
+            wl = WORKLOADS["c3"]
+            k, K, e = wl["k"], wl["K"], wl["e"]
+            N = K ** e
+            params = gp.GfpParams(R[k], k)
+            plan = gp.build_plan(gp.GfpFftField(params, backend="cuda"), K, e,
+                                 checked_roots(gp, params, N))
+            x = gp.vec.uniform(N, params, seed=300, batch=64)
+            y = torch.empty_like(x)
+            t = timed_loop(lambda: gp.fft_tensor(x, plan, out=y), steps, 2, 1, flush, stream)
+            one["c3_split"] = sum(t) / len(t)
+            del x, y
+            k, K = 8, 16
+            N = 1 << 24
+            params = gp.GfpParams(R[k], k)
+            plan = gp.build_plan(gp.GfpFftField(params, backend="cuda"), K, 6,
+                                 checked_roots(gp, params, N))
+            x = gp.vec.uniform(N, params, seed=400)
+            y = torch.empty_like(x)
+            t = timed_loop(lambda: gp.fft_tensor(x, plan, out=y), steps, 2, 1, flush, stream)
+            one["c4_single_gpu_direct"] = sum(t) / len(t)
+            del x, y
+            torch.cuda.empty_cache()
+        except Exception as exc:
+            one["error"] = str(exc)[:300]
+    dist.barrier()
+    if rank == 0:
+        out["same_run_n1_ms"] = one
+        for key in ("c3_split", "c4_sharded", "c4_sharded_peer", "c4_sharded_peer_devsync",
+                    "c4_sharded_peer_flags"):
+            ms = (res.get(key) or {}).get("ms_fwd")
+            base = one.get("c3_split" if key == "c3_split" else "c4_single_gpu_direct")
+            if ms and base:
+                out[key] = {"ms_n": ms, "ms_1": base, "speedup": base / ms,
+                            "parallel_efficiency": base / (ws * ms)}
+    return out
 
 
 def _pinned_em(gp, x):
