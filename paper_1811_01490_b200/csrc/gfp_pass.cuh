@@ -353,11 +353,15 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
     __syncthreads();
 
     // ---- phase C: store in Stockham order (canonicalise on the last pass)
-    // (the k = 32 split DFT leaves X[u0 + 8 u1] in slot u1 + 8 u0)
+    // (the k = 32 split DFT leaves X[u0 + 8 u1] in slot u1 + 8 u0).  On the
+    // first pass (Ns = 1) output u of group j goes to K j + u: lanes take
+    // consecutive u there, so each digit row is written in contiguous runs of
+    // K words (else lanes take consecutive groups: contiguous for Ns >= G)
+    const bool ufast = lNs == 0;
 #pragma unroll 1
     for (int h = 0; h < 2; h++) {
-        const int g = tid & (G - 1);
-        const int u = (tid >> lG) + h * KD;
+        const int g = ufast ? (tid >> LK) + h * (G >> 1) : tid & (G - 1);
+        const int u = ufast ? tid & (K - 1) : (tid >> lG) + h * KD;
         const int64_t j = j0 + g;
         if (j >= M)
             continue;

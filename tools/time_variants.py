@@ -57,6 +57,7 @@ plan3 = gp.build_plan(f16, 32, 4, gp.roots_for(p16, 1 << 20))
 x = gp.vec.uniform(1 << 20, p16, seed=3, batch=8); y = torch.empty_like(x)
 res["c3x8_fwd_ms"] = timeit(lambda: gp.fft_tensor(x, plan3, out=y), 10)
 res["c3_digest"] = dig(y)
+res["c3_pass_ms"] = [round(ms, 4) for _, ms in F.pass_times(plan3, lambda: gp.fft_tensor(x, plan3, out=y))[1]]
 del x, y
 p32 = gp.GfpParams(R[32], 32); f32 = gp.GfpFftField(p32, backend="cuda")
 a = gp.vec.uniform(1 << 22, p32, seed=51); b = gp.vec.uniform(1 << 22, p32, seed=52)
