@@ -135,6 +135,10 @@ int gfp_to_element_major(const uint64_t *src, uint64_t *dst, int64_t n, int k, v
    omega^(N/2) = -1, K = 2k and omega^(N/2k) in {r, 1/r} exactly like the
    reference (GFP_EINVAL otherwise), and builds the device twiddle tables
    (omega^j, j < N/K, and omega^j * N^-1) with the exact device multiply.
+   Every r < 2^64 and k in {4, 8, 16, 32} is accepted: radices with the
+   fast path's headroom (gfp_fast_path_ok) run the lazy-digit pass kernels,
+   the others (e.g. r close to 2^64) radix-2 passes on canonical digits with
+   the reference's element algorithms (gfp_fft_plan_caps = 0; exact, slower).
    Work is enqueued on `stream`; the call synchronises it before returning. */
 int gfp_fft_plan_create(gfp_fft_plan **plan, int k, uint64_t r, int K, int e,
                         const uint64_t *omega, void *stream);

@@ -354,6 +354,44 @@ GFP_HD void dev_gfp_sub(const DX &x, const DY &y, DZ &z, int k, u64 r)
 // ---------------------------------------------------------------------------
 // Canonicalisation of a digit vector with digits in [0, r) and a signed
 // overflow carry C (value = D + C * r^k = D - C mod p), |C| <= 1.
+// x * r^shift on canonical digits, 0 <= shift (taken mod 2k): the
+// reference's gfp_mul_pow_r (gfp_field.py:138-161) -- shift >= k negates
+// first, then B - A with B the up-shifted digits and A the wrapped top
+// digits; a form-B digit r moves one slot up
+template <int KD>
+GFP_D void dev_mul_pow_r(u64 (&a)[KD], int shift, u64 r)
+{
+    u64 A[KD], B[KD];
+    int s = shift % (2 * KD);
+    if (s >= KD) {
+        u64 zero[KD];
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            zero[d] = 0;
+        dev_gfp_sub(zero, a, a, KD, r);
+        s -= KD;
+    }
+    if (s) {
+        const bool formb = a[KD - 1] == r;
+#pragma unroll
+        for (int d = 0; d < KD; d++) {
+            const int src = d - s;
+            B[d] = src >= 0 ? a[src] : 0;
+            A[d] = src < 0 ? a[src + KD] : 0;
+        }
+        if (formb) {
+            // a[k-1] = r lands in A[s-1]; carry it one slot up
+            for (int d = 0; d < KD; d++) {
+                if (d == s - 1)
+                    A[d] -= r;
+                if (d == s)
+                    A[d] += 1;
+            }
+        }
+        dev_gfp_sub(B, A, a, KD, r);
+    }
+}
+
 template <typename DZ>
 GFP_HD void finish_canonical(DZ &z, int k, u64 r, int C)
 {

@@ -257,38 +257,11 @@ __global__ void k_mul_pow_r(const u64 *__restrict__ x, u64 *__restrict__ z, int6
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        u64 a[KD], A[KD], B[KD];
+        u64 a[KD];
 #pragma unroll
         for (int d = 0; d < KD; d++)
             a[d] = x[d * n + i];
-        int s = shift % (2 * KD);
-        if (s >= KD) {
-            u64 zero[KD];
-#pragma unroll
-            for (int d = 0; d < KD; d++)
-                zero[d] = 0;
-            dev_gfp_sub(zero, a, a, KD, r);
-            s -= KD;
-        }
-        if (s) {
-            bool formb = a[KD - 1] == r;
-#pragma unroll
-            for (int d = 0; d < KD; d++) {
-                int src = d - s;
-                B[d] = src >= 0 ? a[src] : 0;
-                A[d] = src < 0 ? a[src + KD] : 0;
-            }
-            if (formb) {
-                // a[k-1] = r lands in A[s-1]; carry it one slot up
-                for (int d = 0; d < KD; d++) {
-                    if (d == s - 1)
-                        A[d] -= r;
-                    if (d == s)
-                        A[d] += 1;
-                }
-            }
-            dev_gfp_sub(B, A, a, KD, r);
-        }
+        dev_mul_pow_r<KD>(a, shift, r);
 #pragma unroll
         for (int d = 0; d < KD; d++)
             z[d * n + i] = a[d];

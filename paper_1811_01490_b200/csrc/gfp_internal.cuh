@@ -140,10 +140,20 @@ struct gfp_fft_plan {
     int64_t last_launches;
     int root_inv;  // omega^(N/2k) == 1/r (a plan built on an inverse root)
     // per-launch timing of the last call (gfp_fft_plan_set_timing)
+    int generic;    // radix without the fast path's headroom: gfp_generic_pass.cu
+    u64 *ninv_dev;  // N^-1 (canonical, device) for the generic path's final scale
     int timing, n_ev;
     cudaEvent_t ev[GFP_MAX_TIMED + 1];
     int ev_pass[GFP_MAX_TIMED];
 };
+
+// the generic-radix transform (gfp_generic_pass.cu): radix-2 passes on
+// canonical digits, in -> out (in may equal out), N^-1 included when inverse;
+// and the element-wise product out = in .* G of [batch][k][N] vectors
+int run_generic(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, int64_t batch, int inverse,
+                cudaStream_t st);
+int generic_pointwise(gfp_fft_plan *p, const u64 *in, const u64 *G, u64 *out, int64_t batch,
+                      cudaStream_t st);
 
 // one radix-K Stockham pass (gfp_pass.cuh), instantiated per k in gfp_pass_k*.cu
 // true when the pass kernels of this plan take element-major I/O (PassIO)

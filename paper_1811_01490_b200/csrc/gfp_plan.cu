@@ -252,6 +252,25 @@ static int run_transform(gfp_fft_plan *p, const u64 *in, u64 *out, u64 *work, co
                          int64_t batch, int inverse, int in_canon, int out_canon,
                          cudaStream_t st, const PassIO *em = nullptr)
 {
+    if (p->generic) {  // canonical digits throughout: the forms do not matter
+        if (em)
+            return GFP_EUNSUPPORTED;
+        int err = GFP_OK;
+        if (pre) {
+            err = generic_pointwise(p, in, pre, work, batch, st);
+            in = work;
+            if (!err && work == out)
+                return GFP_EINVAL;
+            // the transform ping-pongs between out and a second buffer:
+            // the spectra product sits in work, so copy it to out first
+            if (!err) {
+                cudaMemcpyAsync(out, work, sizeof(u64) * (size_t)p->k * p->N * batch,
+                                cudaMemcpyDeviceToDevice, st);
+                in = out;
+            }
+        }
+        return err ? err : run_generic(p, in, out, work, batch, inverse, st);
+    }
     return run_transform2(p, in, out, work, nullptr, nullptr, nullptr, pre, batch, inverse,
                           in_canon, out_canon, st, em);
 }
@@ -283,12 +302,13 @@ int gfp_fft_plan_create(gfp_fft_plan **plan, int k, uint64_t r, int K, int e,
         if (omega[d] > r)
             return GFP_EINVAL;
     RadixConsts rc = make_consts(k, r);
-    if (rc.stages_per_norm <= 0)
-        return GFP_EUNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
     gfp_fft_plan *p = (gfp_fft_plan *)calloc(1, sizeof(gfp_fft_plan));
     if (!p)
         return GFP_ENOMEM;
+    // radices without the fast path's headroom: canonical radix-2 passes
+    // (gfp_generic_pass.cu)
+    p->generic = rc.stages_per_norm <= 0 ? 1 : 0;
     p->k = k;
     p->K = K;
     p->e = e;
@@ -383,11 +403,19 @@ int gfp_fft_plan_create(gfp_fft_plan **plan, int k, uint64_t r, int K, int e,
                                                                            p->M, rc)));
     DISPATCH_FAST_K(k, (k_table_scale<KD><<<grid_for(p->M, 64), 64, 0, st>>>(
                            p->table, d_buf, p->table_ninv, p->M, rc)));
-    DISPATCH_FAST_K(k, (k_table_balance<KD><<<grid_for(p->M, 128), 128, 0, st>>>(p->table, p->M, r)));
-    DISPATCH_FAST_K(k, (k_table_balance<KD><<<grid_for(p->M, 128), 128, 0, st>>>(p->table_ninv, p->M,
-                                                                                r)));
-    err = cuda_status();
-    if (!err) {  // limb-pair tables: the twiddle operand of every pass kernel
+    if (p->generic) {  // canonical table, N^-1 kept for the final scale
+        if (cudaMalloc(&p->ninv_dev, sizeof(u64) * k) != cudaSuccess)
+            err = GFP_ENOMEM;
+        else
+            cudaMemcpyAsync(p->ninv_dev, ninv, sizeof(u64) * k, cudaMemcpyHostToDevice, st);
+    } else {
+        DISPATCH_FAST_K(k, (k_table_balance<KD><<<grid_for(p->M, 128), 128, 0, st>>>(p->table,
+                                                                                    p->M, r)));
+        DISPATCH_FAST_K(k, (k_table_balance<KD><<<grid_for(p->M, 128), 128, 0, st>>>(
+                               p->table_ninv, p->M, r)));
+    }
+    err = err ? err : cuda_status();
+    if (!err && !p->generic) {  // limb-pair tables: the twiddle operand of every pass kernel
         if (cudaMalloc(&p->table_lh, tbytes) != cudaSuccess ||
             cudaMalloc(&p->table_ninv_lh, tbytes) != cudaSuccess) {
             err = GFP_ENOMEM;
@@ -408,6 +436,7 @@ int gfp_fft_plan_create(gfp_fft_plan **plan, int k, uint64_t r, int K, int e,
         cudaFree(p->table_ninv);
         cudaFree(p->table_lh);
         cudaFree(p->table_ninv_lh);
+        cudaFree(p->ninv_dev);
         free(p);
         return err;
     }
@@ -420,6 +449,8 @@ int gfp_fft_twiddle(const gfp_fft_plan *p, const uint64_t *x, uint64_t *out, int
 {
     if (!p || !x || !out || batch < 1 || n < 1 || row0 < 0)
         return GFP_EINVAL;
+    if (p->generic)
+        return GFP_EUNSUPPORTED;
     cudaStream_t st = (cudaStream_t)stream;
     const int lN = ilog2_exact(p->N), lM = ilog2_exact(p->M);
     dim3 grid = grid_for(batch * n, 128);
@@ -448,6 +479,7 @@ int gfp_fft_plan_destroy(gfp_fft_plan *p)
     cudaFree(p->table_lh);
     cudaFree(p->table_ninv_lh);
     cudaFree(p->h_dev);
+    cudaFree(p->ninv_dev);
     for (int i = 0; i <= GFP_MAX_TIMED; i++)
         if (p->ev[i])
             cudaEventDestroy(p->ev[i]);
@@ -574,8 +606,14 @@ int gfp_poly_mul(const gfp_fft_plan *cp, const uint64_t *f, const uint64_t *g, u
         u64 *o = out + b0 * ew;
         // o = DFT(f) and G = DFT(g) in the same launches; the spectra stay
         // balanced lazy digits, only the product is canonicalised
-        err = run_transform2(p, f + b0 * ew, o, scratch, g + b0 * ew, G, scratch_b, nullptr, nb, 0,
-                             1, 0, st);
+        if (p->generic) {
+            err = run_generic(p, f + b0 * ew, o, scratch, nb, 0, st);
+            if (!err)
+                err = run_generic(p, g + b0 * ew, G, scratch_b, nb, 0, st);
+        } else {
+            err = run_transform2(p, f + b0 * ew, o, scratch, g + b0 * ew, G, scratch_b, nullptr,
+                                 nb, 0, 1, 0, st);
+        }
         if (!err)  // o = IDFT(o .* G), the pointwise product fused into pass 0
             err = run_transform(p, o, o, scratch, G, nb, 1, 0, 1, st);
     }

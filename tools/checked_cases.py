@@ -99,6 +99,19 @@ def main():
     # k_pass<16>, k_pass<32>
     fft_case(16, 2, 2, 6)
     fft_case(32, 2, 1, 7)
+    # the generic-radix path (canonical radix-2 passes, k_pass_generic)
+    R[-8] = (1 << 63) + (1 << 34)
+    pg = gp.GfpParams(R[-8], 8)
+    fg = gp.GfpFftField(pg, backend="cuda")
+    om = gp.roots_for(pg, 256)
+    plg = gp.build_plan(fg, 16, 2, om)
+    opg = O.Plan(8, R[-8], 16, 2, np.array(om, dtype=np.uint64), backend="school")
+    xg = O.random_elements(8, 8, R[-8], 256)
+    check("generic radix fwd/inv",
+          np.array_equal(gp.vec.to_host(gp.fft_tensor(gp.vec.to_device(xg, 8), plg)),
+                         opg.forward(xg)) and
+          np.array_equal(gp.vec.to_host(gp.fft_tensor(gp.vec.to_device(xg, 8), plg,
+                                                      inverse=True)), opg.inverse(xg)))
     # element kernels
     for k in (8, 16, 32):
         a = O.random_elements(10 + k, k, R[k], 1000)
