@@ -918,6 +918,29 @@ def extra_configs(args, dev, flush, stream, hbm_peak, imad_peak):
             torch.cuda.empty_cache()
         except Exception as exc:
             res[key] = {"error": str(exc)[:300]}
+    # the scalar drop-in API (one element per call, the reference's
+    # gfp_add / gfp_mul_fft / gfp_mul_pow_r): host-side latency per call
+    try:
+        import random
+        params = gp.GfpParams(R[8], 8)
+        crt = gp.crt_default()
+        rng = random.Random(3)
+        xs = [gp.gfp_encode(params, rng.randrange(params.p)) for _ in range(64)]
+        lat = {}
+        for name, fn in (("gfp_add", lambda a, b: gp.gfp_add(params, a, b)),
+                         ("gfp_mul_pow_r", lambda a, b: gp.gfp_mul_pow_r(params, a, 3)),
+                         ("gfp_mul_bigint", lambda a, b: gp.gfp_mul_bigint(params, a, b)),
+                         ("gfp_mul_fft", lambda a, b: gp.gfp_mul_fft(params, crt, a, b))):
+            for i in range(20):
+                fn(xs[i % 64], xs[(i + 1) % 64])
+            t0 = time.perf_counter()
+            for i in range(400):
+                fn(xs[i % 64], xs[(i + 7) % 64])
+            lat[name + "_us"] = (time.perf_counter() - t0) / 400 * 1e6
+        res["scalar_api"] = dict(lat, note="host wall time per call, k=8 (gfp_scalar_op: one "
+                                           "staged H2D, one kernel, one D2H)")
+    except Exception as exc:
+        res["scalar_api"] = {"error": str(exc)[:300]}
     # the word-prime transform (MontField over P1) and the
     # cyclic convolution, 8 x 2^20 words; HBM roofline of the NTT passes
     # (each radix-16 pass streams 2 x 8 bytes per word)

@@ -80,6 +80,20 @@ int gfp_vec_mul_pow_r(const uint64_t *x, uint64_t *z, int64_t n, int k, uint64_t
 int gfp_vec_mul(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint64_t *z, int64_t n,
                 int k, uint64_t r, void *stream);
 
+/* One element operation on host digit tuples (k <= 128 canonical digits
+   each): the reference's scalar functions in one synchronous call (one H2D
+   through a persistent pinned staging buffer, one kernel, one D2H).
+     op 0  z = x + y          gfp_add        (gfp_field.py:82-109)
+     op 1  z = x - y          gfp_sub        (gfp_field.py:112-135)
+     op 2  z = x r^arg        gfp_mul_pow_r  (gfp_field.py:138-161), 0 <= arg <= 2k
+     op 3  z = x y            gfp_mul_bigint (gfp_mult.py:504-512), direct multiply
+     op 4  z = x y            gfp_mul_fft    (gfp_mult.py:416-501), the mechanism
+                              (GFP_ECONFIG when check_prime_compat fails)
+     op 5  z = x^e            gfp_pow        (gfp_field.py:164-177), e = y[0..arg)
+                              little-endian 64-bit limbs, arg <= 64 */
+int gfp_scalar_op(int op, const uint64_t *x, const uint64_t *y, int64_t arg, uint64_t *z, int k,
+                  uint64_t r, void *stream);
+
 /* Host-buffer element-wise product: x, y, z are element-major host arrays
    uint64[n][k] (the reference's tuple order); H2D, layout conversion,
    gfp_vec_mul, back; synchronous.  The call a reference-side binding makes

@@ -38,6 +38,9 @@ SIGNATURES = {
     "gfp_vec_sub": (_int, [_u64p, _u64p, _u64p, _i64, _int, _u64, _vp]),
     "gfp_vec_mul_pow_r": (_int, [_u64p, _u64p, _i64, _int, _u64, _int, _vp]),
     "gfp_vec_mul": (_int, [_u64p, _u64p, _i64, _u64p, _i64, _int, _u64, _vp]),
+    "gfp_scalar_op": (_int, [_int, ctypes.POINTER(ctypes.c_uint64),
+                             ctypes.POINTER(ctypes.c_uint64), _i64,
+                             ctypes.POINTER(ctypes.c_uint64), _int, _u64, _vp]),
     "gfp_vec_mul_host": (_int, [_u64p, _u64p, _u64p, _i64, _int, _u64, _vp]),
     "gfp_vec_mul_crt": (_int, [_u64p, _u64p, _i64, _u64p, _i64, _int, _u64, _vp]),
     "gfp_vec_mul_crt_profile": (_int, [_u64p, _u64p, _i64, _u64p, _i64, _int, _u64,

@@ -741,3 +741,86 @@ int gfp_to_element_major(const uint64_t *src, uint64_t *dst, int64_t n, int k, v
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// One element operation on host digit tuples (the reference's scalar API:
+// gfp_add, gfp_sub, gfp_mul_pow_r, gfp_mul_fft / gfp_mul_bigint, gfp_pow):
+// one H2D of the operands through a persistent pinned staging buffer, one
+// kernel, one D2H, one stream synchronisation -- instead of a tensor
+// allocation and two synchronising copies per operand in the Python layer.
+#include <mutex>
+
+namespace {
+struct ScalarStage {
+    u64 *host = nullptr;  // pinned: [x k][y k][e limbs][z k]
+    u64 *dev = nullptr;
+};
+constexpr int SCALAR_WORDS = 3 * 128 + 64;  // x, y, z (k <= 128) + 64 exponent limbs
+ScalarStage g_scalar[64];
+std::mutex g_scalar_mu;
+}  // namespace
+
+extern "C" int gfp_scalar_op(int op, const uint64_t *x, const uint64_t *y, int64_t arg,
+                             uint64_t *z, int k, uint64_t r, void *stream)
+{
+    int e = check_kr(k, r);
+    if (e)
+        return e;
+    if (!x || !z || op < 0 || op > 5 || ((op <= 1 || op == 3 || op == 4 || op == 5) && !y))
+        return GFP_EINVAL;
+    if (op == 2 && (arg < 0 || arg > 2 * k))
+        return GFP_EINVAL;
+    if (op == 5 && (arg < 0 || arg > 64))
+        return GFP_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_scalar_mu);
+    ScalarStage &S = g_scalar[dev & 63];
+    if (!S.host) {
+        if (cudaMallocHost(&S.host, sizeof(u64) * SCALAR_WORDS) != cudaSuccess ||
+            cudaMalloc(&S.dev, sizeof(u64) * SCALAR_WORDS) != cudaSuccess) {
+            cudaGetLastError();
+            return GFP_ENOMEM;
+        }
+    }
+    u64 *hx = S.host, *hy = hx + 128, *he = hy + 128, *hz = he + 64;
+    u64 *dx = S.dev, *dy = dx + 128, *de = dy + 128, *dz = de + 64;
+    memcpy(hx, x, sizeof(u64) * k);
+    const int ny = op == 5 ? (int)arg : (op == 2 ? 0 : k);
+    if (ny)
+        memcpy(op == 5 ? he : hy, y, sizeof(u64) * ny);
+    cudaMemcpyAsync(dx, hx, sizeof(u64) * (128 + 128 + 64), cudaMemcpyHostToDevice, st);
+    const RadixConsts rc = make_consts(k, r);
+    switch (op) {
+    case 0:
+    case 1:
+        DISPATCH_K(k, (k_add<KD><<<1, 32, 0, st>>>(dx, dy, dz, 1, r, op)));
+        break;
+    case 2:
+        DISPATCH_K(k, (k_mul_pow_r<KD><<<1, 32, 0, st>>>(dx, dz, 1, r, (int)arg)));
+        break;
+    case 3:
+        e = gfp_vec_mul(dx, dy, 1, dz, 1, k, r, st);
+        break;
+    case 4:
+        e = gfp_vec_mul_crt(dx, dy, 1, dz, 1, k, r, st);
+        break;
+    default: {
+        int nbits = 0;
+        for (int i = (int)arg - 1; i >= 0; i--)
+            if (he[i]) {
+                nbits = 64 * i + 64 - __builtin_clzll(he[i]);
+                break;
+            }
+        DISPATCH_K(k, (k_pow<KD><<<1, 32, 0, st>>>(dx, de, nbits, dz, 1, rc)));
+    }
+    }
+    if (e)
+        return e;
+    cudaMemcpyAsync(hz, dz, sizeof(u64) * k, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess)
+        return GFP_ECUDA;
+    memcpy(z, hz, sizeof(u64) * k);
+    return cuda_status();
+}

@@ -109,6 +109,9 @@ def add_step_profile(profile, cycles, seconds):
 def _mul_device(params, x, y, profile=None, mechanism=False):
     if len(x) != params.k or len(y) != params.k:
         raise ValueError("element must have k digits")
+    if profile is None and params.k <= 128:  # one staged call (gfp_scalar_op)
+        from .gfp_field import OP_MUL, OP_MUL_CRT, scalar_op
+        return scalar_op(OP_MUL_CRT if mechanism and params.k <= 64 else OP_MUL, params, x, y)
     a = vec.to_device([x], params.k)
     b = vec.to_device([y], params.k)
     # mechanism: the reference's two-prime convolution + CRT + LHC route
