@@ -360,8 +360,9 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
     const bool ufast = lNs == 0;
 #pragma unroll 1
     for (int h = 0; h < 2; h++) {
-        const int g = ufast ? (tid >> LK) + h * (G >> 1) : tid & (G - 1);
-        const int u = ufast ? tid & (K - 1) : (tid >> lG) + h * KD;
+        const int idx = tid + h * (G * KD);  // (g, u) pair over both iterations: G K outputs
+        const int g = ufast ? idx >> LK : tid & (G - 1);
+        const int u = ufast ? idx & (K - 1) : (tid >> lG) + h * KD;
         const int64_t j = j0 + g;
         if (j >= M)
             continue;
