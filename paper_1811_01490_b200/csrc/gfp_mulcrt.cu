@@ -24,6 +24,8 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <mutex>
+
 #include "gfp_internal.cuh"
 #include "gfpfft.h"
 
@@ -360,8 +362,22 @@ static int mul_crt_run(const uint64_t *x, const uint64_t *y, int64_t y_inc, uint
         return GFP_EUNSUPPORTED;
     if (n <= 0)
         return GFP_OK;
+    // the plan constants depend on k only: built once per k (log2 k < 7)
+    static CrtConsts cache[7];
+    static bool have[7] = {false, false, false, false, false, false, false};
+    static std::mutex mu;
+    int lk = 0;
+    while ((1 << lk) < k)
+        lk++;
     CrtConsts C;
-    make_crt_consts(k, C);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!have[lk]) {
+            make_crt_consts(k, cache[lk]);
+            have[lk] = true;
+        }
+        C = cache[lk];
+    }
     const RadixConsts rc = make_consts(k, r);
     const dim3 grid = grid_for(n, 128);
 #define MUL_CRT(KK)                                                                           \
