@@ -283,6 +283,22 @@ def task_c3_idx63(_):
                         "seconds": time.time() - t0}
 
 
+def task_c3_idx(b):
+    # transform b of the C3 batch: draws [b 2^20, (b + 1) 2^20) of one
+    # Random(3) stream, forward by the reference's dft_general
+    N = 1 << 20
+    params, field, plan = field_plan(16, N)
+    rng = random.Random(3)
+    for _ in range(b * N):
+        rng.randrange(params.p)
+    v = draws(params, 3, N, rng=rng)
+    t0 = time.time()
+    w = fft.dft_general(list(v), plan, field)
+    return "c3_idx%d" % b, {"k": 16, "N": N, "seed": 3, "batch_index": b,
+                            "input": digest(v), "forward": digest(w),
+                            "seconds": time.time() - t0}
+
+
 def task_c4_prefix(_):
     N = 1 << 16
     params, field, plan = field_plan(8, N)
@@ -371,6 +387,7 @@ def main():
                     help="also run C3[0], C5-FFT and the full C4 forward")
     ap.add_argument("--only", default="")
     ap.add_argument("--jobs", type=int, default=os.cpu_count())
+    ap.add_argument("--c3", default="", help="extra C3 batch indices, comma-separated")
     args = ap.parse_args()
     tasks = [(task_ops, None), (task_fft_small, None), (task_gfpv, None), (task_word, None),
              (task_c1, None),
@@ -383,6 +400,8 @@ def main():
     if args.big:
         tasks = [(task_c4_full, None), (task_c3_idx0, None), (task_c3_idx63, None),
                  (task_c5_full, None), (task_c5_fft, None)] + tasks
+    if args.c3:
+        tasks = [(task_c3_idx, int(b)) for b in args.c3.split(",")] + tasks
     if args.only:
         keep = set(args.only.split(","))
         tasks = [t for t in tasks if t[0].__name__ in keep]
