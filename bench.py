@@ -558,7 +558,7 @@ def run_ours(args, ws, rank, local):
                                           "Karatsuba): the integer-pipe utilisation"},
                      "traffic": traffic,
                      "traffic_note": "dram read+write bytes per step, ncu --set full over the "
-                                     "step's pass launches, from the committed capture "
+                                     "step's pass launches, from the committed round-2 capture "
                                      "profiles/ncu_traffic.json (not this run)",
                      "regime": "latency-bound, L2-resident (4 MiB operands; one wave of "
                                "256 CTAs per pass)",
