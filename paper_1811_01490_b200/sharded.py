@@ -9,8 +9,12 @@ GPUs).  With n = N2 n1 + n2 and k = k1 + N1 k2:
   1. column DFTs of size N1 on the local columns n2 (batched k_pass kernels);
   2. the inter-stage twiddle w_N^(n2 k1) (gfp_fft_twiddle, the D_{N1,N2}
      stage of the reference's tensor formula, fft.py:62-103);
-  3. the transpose as ONE all-to-all (torch.distributed.all_to_all_single,
-     NCCL over NVLink/NVSwitch on GPUs, gloo in the CPU tests);
+  3. the transpose: ONE all-to-all (torch.distributed.all_to_all_single,
+     NCCL over NVLink/NVSwitch on GPUs, gloo in the CPU tests), or -- with
+     use_peer_exchange() -- direct stores into every rank's receive buffer
+     over CUDA IPC peer pointers, fused into the column DFTs' last pass
+     (PeerExchange: host barriers, NCCL barriers or device-side
+     release/acquire completion flags between the ranks' kernels);
   4. row DFTs of size N2 on the local rows k1.
 
 Layouts (digit-major, like every device vector of the package):
@@ -40,6 +44,10 @@ def _u64(t):
 
 
 class ShardedFFT:
+    """One rank's share of an N1 N2-point transform (see the module
+    docstring): forward(cols) -> rows, inverse(rows) -> cols; the exchange
+    path in use is recorded in exchange_path."""
+
     def __init__(self, ops, k, N1, N2, rank=0, world=1, group=None):
         if N1 % world or N2 % world:
             raise ValueError("N1 and N2 must be divisible by the number of ranks")
