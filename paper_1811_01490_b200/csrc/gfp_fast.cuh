@@ -222,7 +222,7 @@ GFP_D int sign_win(int v, int neg_one) { return GFP_NEG_WIN_ALU ? cond_neg(v, ne
 //
 // dst != nullptr: each output digit is stored to dst[m] as soon as it is
 // final instead of being kept in f (frees registers in the pass kernel).
-template <int KD, int SPARSE, bool STORE = false>
+template <int KD, int SPARSE, bool STORE = false, int DST = 1>
 GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&xs)[KD],
                           const int (&yl)[KD], const int (&yh)[KD], const int (&ys)[KD],
                           i64 (&f)[KD], const RadixConsts &rc, i64 *dst = nullptr)
@@ -278,7 +278,7 @@ GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&
         i64 v;
         if (cr.column(m, LL, MID, HH, rc, v)) {
             if (STORE)
-                dst[m] = v;
+                dst[m * DST] = v;
             else
                 f[m] = v;
         }
@@ -287,7 +287,7 @@ GFP_D void fast_mul_limbs(const int (&xl)[KD], const int (&xh)[KD], const int (&
     cr.finish(rc, o0, o1);
     if (STORE) {
         dst[0] = o0;
-        dst[1] = o1;
+        dst[DST] = o1;
     } else {
         f[0] = o0;
         f[1] = o1;
@@ -324,8 +324,10 @@ GFP_D void fast_mul_lazy(const i64 (&x)[KD], const i64 (&y)[KD], i64 (&f)[KD],
 }
 
 // the same product with y given as pre-split limb pairs (l | h << 32 per
-// digit, the plan's limb tables): no split work for the twiddle operand
-template <int KD, int SPARSE, bool STORE = false>
+// digit, the plan's limb tables): no split work for the twiddle operand.
+// DST: stride in words between the stored digits (STORE; 32 for the
+// digit-major tiles of k_pass44t)
+template <int KD, int SPARSE, bool STORE = false, int DST = 1>
 GFP_D void fast_mul_lazy_ylimbs(const i64 (&x)[KD], const u64 (&ylh)[KD], i64 (&f)[KD],
                                 const RadixConsts &rc, unsigned negx = 0, i64 *dst = nullptr)
 {
@@ -343,7 +345,7 @@ GFP_D void fast_mul_lazy_ylimbs(const i64 (&x)[KD], const u64 (&ylh)[KD], i64 (&
         yh[i] = (int)(unsigned)(ylh[i] >> 32);
         ys[i] = yl[i] + yh[i];
     }
-    fast_mul_limbs<KD, SPARSE, STORE>(xl, xh, xs, yl, yh, ys, f, rc, dst);
+    fast_mul_limbs<KD, SPARSE, STORE, DST>(xl, xh, xs, yl, yh, ys, f, rc, dst);
 }
 
 // x * y with the y limbs in a shared-memory column (this thread's int2

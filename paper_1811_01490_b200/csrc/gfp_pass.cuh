@@ -11,6 +11,7 @@
 #include "gfp_internal.cuh"
 #include "gfp_fast.cuh"
 #include "gfp_pass44.cuh"
+#include "gfp_pass44t.cuh"
 
 // k values whose pass multiply keeps the twiddle limbs in shared memory
 // (fast_mul_window_store) instead of registers
@@ -514,6 +515,11 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
                              em, G, A);
     if (err)
         return err;
+    // large k = 8 transforms: the TMA form of the pass for every pass it takes
+    if (pass44_enabled(KD, A.rc) &&
+        p44t_takes(A, p->M, ((p->M + 31) / 32) * (in2 ? 2 * batch : batch)) &&
+        launch_pass44t<KD>(A, p->M, in2 ? 2 * batch : batch, st))
+        return cuda_status();
     if (launch_pass44<KD>(A, p->M, in2 ? 2 * batch : batch, st))
         return cuda_status();
     if (A.in_em || A.out_em || A.ft_lh || A.xg)

@@ -1,0 +1,359 @@
+// gfp_pass44t.cuh -- the k = 8 radix-16 Stockham pass for large transforms
+// with TMA tile movement (sm_100a: cp.async.bulk.tensor + mbarrier).
+//
+// Same pass and the same arithmetic as k_pass44 (gfp_pass44.cuh; the
+// reference's dft_general level, fft.py:298-360, with the level twiddle split
+// r^a omega^b of fft.py:84-103), for the passes that carry the bulk of a large
+// transform: not the first pass (Ns >= 32), digit-major input and output,
+// every group of the CTA present (M % 32 == 0).  What changes is how the
+// digit rows move:
+//
+//   * the vectors are 3-D tensors [batch][k][N] of u64; one TMA box
+//     {32 columns, k rows, 1} is the 2 KB tile "element t of 32 consecutive
+//     groups, all digits".  Lane 0 of warp w issues the four tile loads of the
+//     warp's elements t = w + 4 i at kernel start -- 8 KB in flight per warp
+//     with no registers or address arithmetic spent on them (the LDG form
+//     spends ~65 of the pass's ~1020 instructions per element on it and has
+//     one element's rows in flight) -- each completing on its own mbarrier;
+//   * shared memory holds the 16 tiles digit-major ([t][d][lane], 32 KB, no
+//     padding: a thread only ever touches its own column, and a warp's
+//     64-bit accesses to one digit row are conflict-free).  The rotation r^a
+//     is the row index of the tile read, the product digits go back to the
+//     same tile, stage 1 / stage 2 exchange through the tiles in place;
+//   * the outputs X[u0 + 4 u1] of warp u0 are written back into the warp's
+//     own four tiles and leave as four TMA box stores (Ns >= 32: the 32
+//     groups' outputs are 32 consecutive columns).
+#pragma once
+#include <cuda.h>
+
+#include "gfp_pass44.cuh"
+
+#ifndef P44_TMA
+#define P44_TMA 1  // 0: large transforms stay on k_pass44<NW = 4> (A/B builds)
+#endif
+#ifndef P44T_MINB
+#define P44T_MINB 5  // CTAs per SM the kernel is register-bounded for (32 KB tiles each)
+#endif
+#ifndef P44T_EVICT_FIRST
+#define P44T_EVICT_FIRST 1  // streamed tiles carry an L2 evict-first policy (tables stay)
+#endif
+
+// tensor maps of one pass launch: the two vector sets' inputs and outputs
+struct PassTma {
+    CUtensorMap in, in2, out, out2;
+};
+
+namespace p44t {
+
+GFP_D unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+GFP_D void mbar_init(u64 *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+GFP_D void mbar_expect_tx(u64 *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+// wait for the barrier's phase `parity` to complete (try_wait suspends the
+// thread for a bounded time per attempt)
+GFP_D void mbar_wait(u64 *bar, unsigned parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "P44T_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra P44T_DONE;\n"
+        "bra P44T_WAIT;\n"
+        "P44T_DONE:\n"
+        "}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+GFP_D u64 evict_first_policy()
+{
+    u64 pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// box {c0 .. c0 + 31, all rows, batch c2} -> dst, completion on bar
+GFP_D void tma_load(void *dst, const CUtensorMap *map, u64 *bar, int c0, int c2, u64 pol)
+{
+#if P44T_EVICT_FIRST
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(0), "r"(c2), "l"(pol)
+        : "memory");
+#else
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(0), "r"(c2)
+        : "memory");
+#endif
+}
+GFP_D void tma_store(const CUtensorMap *map, const void *src, int c0, int c2, u64 pol)
+{
+#if P44T_EVICT_FIRST
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group.L2::cache_hint"
+                 " [%0, {%2, %3, %4}], [%1], %5;" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(0), "r"(c2), "l"(pol)
+                 : "memory");
+#else
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group"
+                 " [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(0), "r"(c2)
+                 : "memory");
+#endif
+}
+
+}  // namespace p44t
+
+template <int KD, int SPARSE, bool INV>
+__global__ void __launch_bounds__(128, P44T_MINB)
+    k_pass44t(const __grid_constant__ PassArgs A, const __grid_constant__ PassTma T)
+{
+    static_assert(KD == 8, "radix 4 x 4 pass is for K = 16");
+    constexpr int K = 2 * KD;
+    constexpr int TILE = KD * 32;  // words of one tile: [d][lane]
+    __shared__ __align__(128) i64 sm[K * TILE];
+    __shared__ __align__(8) u64 bar[K];
+    const int lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;  // elements t = w + 4 i; t1 in stage 1, u0 in stage 2
+
+    int bidx = blockIdx.y;
+    const CUtensorMap *tin = &T.in, *tout = &T.out;
+    if (bidx >= A.batch) {
+        bidx -= (int)A.batch;
+        tin = &T.in2;
+        tout = &T.out2;
+    }
+    const int lN = A.lN, lM = A.lM, lNs = A.lNs;
+    const int64_t N = (int64_t)1 << lN, M = (int64_t)1 << lM;
+    const int64_t nsmask = ((int64_t)1 << lNs) - 1;
+    const RadixConsts rc = A.rc;
+    const int j0 = blockIdx.x * 32;  // M % 32 == 0: every lane has a group
+    const int64_t j = j0 + lane;
+
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int t = 0; t < K; t++)
+            p44t::mbar_init(&bar[t], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // programmatic dependent launch (see k_pass44): the previous pass's
+    // writes are visible after the wait, before the first tile load
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const u64 pol = p44t::evict_first_policy();
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int t = w + 4 * i;
+            p44t::mbar_expect_tx(&bar[t], TILE * 8);
+            p44t::tma_load(sm + t * TILE, tin, &bar[t], j0 + (t << lM), bidx, pol);
+        }
+    }
+
+    // ---- phase A: element t = w + 4 i of the lane's group times omega^E =
+    // r^a omega^b; r^a is the row the digit is read from (and a sign folded
+    // into the multiply's limb split), omega^b one general multiply whose
+    // digits go back to the tile as they become final
+#pragma unroll 1
+    for (int i = 0; i < 4; i++) {
+        const int t = w + 4 * i;
+        i64 *tile = sm + GFP_IDX(t * TILE + lane, K * TILE);
+        const p44::Twiddle tw =
+            p44::twiddle_of<KD>(t, j, nsmask, lM, lNs, N, M, A.neg_exp, A.root_inv);
+        // warp-uniform multiply: lanes with b = 0 multiply by table[0] = 1
+        const bool mul_tw = __any_sync(FULL_MASK, tw.b || A.scale);
+        p44t::mbar_wait(&bar[t], 0);
+        i64 x[KD], f[KD];
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            x[d] = tile[((d - tw.as) & (KD - 1)) * 32];
+        if (mul_tw) {
+            const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(
+                A.table_lh + GFP_IDX(tw.b, M) * KD);
+            u64 ylh[KD];
+#pragma unroll
+            for (int d = 0; d < KD; d += 2) {
+                const ulonglong2 v = __ldg(tp + d / 2);
+                ylh[d] = v.x;
+                ylh[d + 1] = v.y;
+            }
+            fast_mul_lazy_ylimbs<KD, SPARSE, true, 32>(x, ylh, f, rc, tw.negx, tile);
+        } else {  // r^a alone (t = 0: the identity)
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                tile[d * 32] = ((tw.negx >> d) & 1u) ? -x[d] : x[d];
+        }
+    }
+
+    GFP_JITTER(1);
+    // ---- stage 1 (t1 = w): 4-point DFT over t2 of tiles t1 + 4 t2, outputs
+    // u0 back into tiles t1 + 4 u0 -- the same four tiles, this thread's own
+    // phase-A columns: no barrier
+    i64 e[4][KD];
+#pragma unroll
+    for (int t2 = 0; t2 < 4; t2++) {
+        const i64 *tile = sm + GFP_IDX((w + 4 * t2) * TILE + lane, K * TILE);
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            e[t2][d] = tile[d * 32];
+    }
+    p44::dft4<KD, INV, 0>(e[0], e[1], e[2], e[3]);
+#pragma unroll
+    for (int u0 = 0; u0 < 4; u0++) {
+        i64 *tile = sm + GFP_IDX((4 * u0 + w) * TILE + lane, K * TILE);
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            tile[d * 32] = e[u0][d];
+    }
+    GFP_JITTER(2);
+    __syncthreads();
+
+    // ---- stage 2 (u0 = w): gather Y[t1][u0] from tiles 4 u0 + t1, twiddle
+    // rho^(t1 u0) as a compile-time rotation, DFT over t1
+    const int u0 = w;
+#pragma unroll
+    for (int t1 = 0; t1 < 4; t1++) {
+        const i64 *tile = sm + GFP_IDX((4 * u0 + t1) * TILE + lane, K * TILE);
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            e[t1][d] = tile[d * 32];
+    }
+    switch (u0) {
+    case 0: p44::dft4<KD, INV, 0>(e[0], e[1], e[2], e[3]); break;
+    case 1: p44::dft4<KD, INV, 1>(e[0], e[1], e[2], e[3]); break;
+    case 2: p44::dft4<KD, INV, 2>(e[0], e[1], e[2], e[3]); break;
+    default: p44::dft4<KD, INV, 3>(e[0], e[1], e[2], e[3]); break;
+    }
+    // one balanced normalisation per output, the canonical form on the last
+    // pass; X[u0 + 4 u1] = e[u1] goes back to tile 4 u0 + u1 (this thread's
+    // own column of the warp's own tiles)
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        p44::normalize_el<KD, SPARSE>(e[q], rc);
+        i64 *tile = sm + GFP_IDX((4 * u0 + q) * TILE + lane, K * TILE);
+        if (A.canon) {
+            u64 c[KD];
+            lazy_to_canonical_bf<KD>(e[q], c, rc);
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                tile[d * 32] = (i64)c[d];
+        } else {
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                tile[d * 32] = e[q][d];
+        }
+    }
+    // generic-proxy writes -> async proxy (TMA) reads
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+        // output u of group j at (j / Ns) Ns K + (j mod Ns) + u Ns; Ns >= 32
+        // and j0 % 32 == 0: the warp's 32 groups are 32 consecutive columns
+        const int64_t base = (((int64_t)j0 >> lNs) << (lNs + 4)) + (j0 & nsmask);
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+            p44t::tma_store(tout, sm + (4 * u0 + q) * TILE,
+                            (int)(base + ((int64_t)(u0 + 4 * q) << lNs)), bidx, pol);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        // the tiles must stay until the stores have read them
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link
+// dependency on libcuda); nullptr when the driver does not offer it
+typedef CUresult (*p44t_encode_fn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                   const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                   const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static inline p44t_encode_fn p44t_encoder()
+{
+    static p44t_encode_fn fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+        }
+        return (p44t_encode_fn)p;
+    }();
+    return fn;
+}
+
+// tensor map of a digit-major vector set: [batch][k][N] u64, box {32, k, 1}
+static inline bool p44t_make_map(CUtensorMap *m, const u64 *base, int64_t N, int k, int64_t batch,
+                                 int64_t batch_stride)
+{
+    p44t_encode_fn enc = p44t_encoder();
+    if (!enc || ((uintptr_t)base & 15))
+        return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)k, (cuuint64_t)batch};
+    const cuuint64_t strides[2] = {(cuuint64_t)N * 8, (cuuint64_t)batch_stride * 8};
+    const cuuint32_t box[3] = {32, (cuuint32_t)k, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, (void *)base, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+}
+
+// the passes k_pass44t takes: a large transform's (grid of at least four
+// waves, the NW = 4 regime of k_pass44) digit-major passes after the first
+static inline bool p44t_takes(const PassArgs &A, int64_t M, int64_t ctas)
+{
+    return P44_TMA && ctas >= 4 * (int64_t)num_sms() && (M & 31) == 0 && A.lNs >= 5 &&
+           A.lN <= 30 && !A.in_em && !A.out_em && !A.ft_lh && !A.xg && !A.pre && !A.in_canon;
+}
+
+// returns 1 when the pass was launched
+template <int KD>
+static int launch_pass44t(const PassArgs &A, int64_t M, int64_t nsets, cudaStream_t st)
+{
+    if constexpr (KD != 8) {
+        return 0;
+    } else {
+        PassTma T;
+        const int64_t N = (int64_t)1 << A.lN;
+        if (!p44t_make_map(&T.in, A.in, N, KD, A.batch, A.batch_stride) ||
+            !p44t_make_map(&T.out, A.out, N, KD, A.batch, A.batch_stride))
+            return 0;
+        T.in2 = T.in;
+        T.out2 = T.out;
+        if (A.in2 && (!p44t_make_map(&T.in2, A.in2, N, KD, A.batch, A.batch_stride) ||
+                      !p44t_make_map(&T.out2, A.out2, N, KD, A.batch, A.batch_stride)))
+            return 0;
+        void (*kern)(const PassArgs, const PassTma) = nullptr;
+        const bool inv = A.rot_inv != 0;
+        if (A.rc.p3_ok)
+            kern = inv ? k_pass44t<KD, 3, true> : k_pass44t<KD, 3, false>;
+        else if (A.rc.p2_ok)
+            kern = inv ? k_pass44t<KD, 2, true> : k_pass44t<KD, 2, false>;
+        else
+            kern = inv ? k_pass44t<KD, 0, true> : k_pass44t<KD, 0, false>;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(M / 32), (unsigned)nsets);
+        cfg.blockDim = dim3(128);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, A, T);
+        return 1;
+    }
+}
