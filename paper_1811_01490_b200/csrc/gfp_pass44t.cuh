@@ -4,8 +4,9 @@
 // Same pass and the same arithmetic as k_pass44 (gfp_pass44.cuh; the
 // reference's dft_general level, fft.py:298-360, with the level twiddle split
 // r^a omega^b of fft.py:84-103), for the passes that carry the bulk of a large
-// transform: not the first pass (Ns >= 32), digit-major input and output,
-// every group of the CTA present (M % 32 == 0).  What changes is how the
+// transform: not the first pass (Ns >= 16), digit-major input and output,
+// every group of the CTA present (M % 32 == 0); NW warps per CTA as in
+// k_pass44 (4 for grids that fill the GPU, 8 / 16 for small transforms).  What changes is how the
 // digit rows move:
 //
 //   * the vectors are 3-D tensors [batch][k][N] of u64; one TMA box
@@ -22,7 +23,7 @@
 //     same tile, stage 1 / stage 2 exchange through the tiles in place;
 //   * the outputs X[u0 + 4 u1] of warp u0 are written back into the warp's
 //     own four tiles and leave as four TMA box stores (Ns >= 32: the 32
-//     groups' outputs are 32 consecutive columns).
+//     groups' outputs are 32 consecutive columns; Ns = 16: two boxes of 16).
 #pragma once
 #include <cuda.h>
 
@@ -40,7 +41,8 @@
 
 // tensor maps of one pass launch: the two vector sets' inputs and outputs
 struct PassTma {
-    CUtensorMap in, in2, out, out2;
+    CUtensorMap in, in2, out, out2;  // box {32, k, 1}
+    CUtensorMap out16, out2_16;      // box {16, k, 1}: the stores of the Ns = 16 pass
 };
 
 namespace p44t {
@@ -114,24 +116,26 @@ GFP_D void tma_store(const CUtensorMap *map, const void *src, int c0, int c2, u6
 
 }  // namespace p44t
 
-template <int KD, int SPARSE, bool INV>
-__global__ void __launch_bounds__(128, P44T_MINB)
+template <int KD, int SPARSE, bool INV, int NW>
+__global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1)
     k_pass44t(const __grid_constant__ PassArgs A, const __grid_constant__ PassTma T)
 {
     static_assert(KD == 8, "radix 4 x 4 pass is for K = 16");
     constexpr int K = 2 * KD;
     constexpr int TILE = KD * 32;  // words of one tile: [d][lane]
+    constexpr int EPT = K / NW;    // phase-A elements per thread
     __shared__ __align__(128) i64 sm[K * TILE];
     __shared__ __align__(8) u64 bar[K];
     const int lane = threadIdx.x & 31;
-    const int w = threadIdx.x >> 5;  // elements t = w + 4 i; t1 in stage 1, u0 in stage 2
+    const int w = threadIdx.x >> 5;  // elements t = w + NW i
 
     int bidx = blockIdx.y;
-    const CUtensorMap *tin = &T.in, *tout = &T.out;
+    const CUtensorMap *tin = &T.in, *tout = &T.out, *tout16 = &T.out16;
     if (bidx >= A.batch) {
         bidx -= (int)A.batch;
         tin = &T.in2;
         tout = &T.out2;
+        tout16 = &T.out2_16;
     }
     const int lN = A.lN, lM = A.lM, lNs = A.lNs;
     const int64_t N = (int64_t)1 << lN, M = (int64_t)1 << lM;
@@ -154,20 +158,20 @@ __global__ void __launch_bounds__(128, P44T_MINB)
     const u64 pol = p44t::evict_first_policy();
     if (lane == 0) {
 #pragma unroll
-        for (int i = 0; i < 4; i++) {
-            const int t = w + 4 * i;
+        for (int i = 0; i < EPT; i++) {
+            const int t = w + NW * i;
             p44t::mbar_expect_tx(&bar[t], TILE * 8);
             p44t::tma_load(sm + t * TILE, tin, &bar[t], j0 + (t << lM), bidx, pol);
         }
     }
 
-    // ---- phase A: element t = w + 4 i of the lane's group times omega^E =
+    // ---- phase A: element t = w + NW i of the lane's group times omega^E =
     // r^a omega^b; r^a is the row the digit is read from (and a sign folded
     // into the multiply's limb split), omega^b one general multiply whose
     // digits go back to the tile as they become final
 #pragma unroll 1
-    for (int i = 0; i < 4; i++) {
-        const int t = w + 4 * i;
+    for (int i = 0; i < EPT; i++) {
+        const int t = w + NW * i;
         i64 *tile = sm + GFP_IDX(t * TILE + lane, K * TILE);
         const p44::Twiddle tw =
             p44::twiddle_of<KD>(t, j, nsmask, lM, lNs, N, M, A.neg_exp, A.root_inv);
@@ -197,31 +201,39 @@ __global__ void __launch_bounds__(128, P44T_MINB)
     }
 
     GFP_JITTER(1);
-    // ---- stage 1 (t1 = w): 4-point DFT over t2 of tiles t1 + 4 t2, outputs
-    // u0 back into tiles t1 + 4 u0 -- the same four tiles, this thread's own
-    // phase-A columns: no barrier
+    // ---- stage 1 (warps w < 4, t1 = w): 4-point DFT over t2 of tiles
+    // t1 + 4 t2, outputs u0 back into tiles t1 + 4 u0 -- the same four tiles.
+    // With NW = 4 they are this thread's own phase-A columns: no barrier.
     i64 e[4][KD];
+    if (NW > 4)
+        __syncthreads();
+    if (w < 4) {
 #pragma unroll
-    for (int t2 = 0; t2 < 4; t2++) {
-        const i64 *tile = sm + GFP_IDX((w + 4 * t2) * TILE + lane, K * TILE);
+        for (int t2 = 0; t2 < 4; t2++) {
+            const i64 *tile = sm + GFP_IDX((w + 4 * t2) * TILE + lane, K * TILE);
 #pragma unroll
-        for (int d = 0; d < KD; d++)
-            e[t2][d] = tile[d * 32];
-    }
-    p44::dft4<KD, INV, 0>(e[0], e[1], e[2], e[3]);
+            for (int d = 0; d < KD; d++)
+                e[t2][d] = tile[d * 32];
+        }
+        p44::dft4<KD, INV, 0>(e[0], e[1], e[2], e[3]);
 #pragma unroll
-    for (int u0 = 0; u0 < 4; u0++) {
-        i64 *tile = sm + GFP_IDX((4 * u0 + w) * TILE + lane, K * TILE);
+        for (int u0 = 0; u0 < 4; u0++) {
+            i64 *tile = sm + GFP_IDX((4 * u0 + w) * TILE + lane, K * TILE);
 #pragma unroll
-        for (int d = 0; d < KD; d++)
-            tile[d * 32] = e[u0][d];
+            for (int d = 0; d < KD; d++)
+                tile[d * 32] = e[u0][d];
+        }
     }
     GFP_JITTER(2);
     __syncthreads();
 
-    // ---- stage 2 (u0 = w): gather Y[t1][u0] from tiles 4 u0 + t1, twiddle
-    // rho^(t1 u0) as a compile-time rotation, DFT over t1
-    const int u0 = w;
+    // ---- stage 2 over SPL = NW / 4 warps per u0: every warp gathers
+    // Y[t1][u0] from tiles 4 u0 + t1, applies rho^(t1 u0) as a compile-time
+    // rotation and runs the (cheap, lazy) DFT over t1, then normalises and
+    // stores only its NU = 4 / SPL outputs u1 in [h NU, h NU + NU)
+    constexpr int SPL = NW / 4, NU = 4 / SPL;
+    const int u0 = w & 3;
+    const int h = w >> 2;
 #pragma unroll
     for (int t1 = 0; t1 < 4; t1++) {
         const i64 *tile = sm + GFP_IDX((4 * u0 + t1) * TILE + lane, K * TILE);
@@ -235,36 +247,68 @@ __global__ void __launch_bounds__(128, P44T_MINB)
     case 2: p44::dft4<KD, INV, 2>(e[0], e[1], e[2], e[3]); break;
     default: p44::dft4<KD, INV, 3>(e[0], e[1], e[2], e[3]); break;
     }
-    // one balanced normalisation per output, the canonical form on the last
-    // pass; X[u0 + 4 u1] = e[u1] goes back to tile 4 u0 + u1 (this thread's
-    // own column of the warp's own tiles)
+    if (SPL > 1) {
+        if (h > 0) {  // this warp's outputs into e[0 .. NU-1] (static indices)
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
+            for (int q = 0; q < NU; q++) {
+#pragma unroll
+                for (int d = 0; d < KD; d++) {
+                    i64 v = e[q][d];
+#pragma unroll
+                    for (int hh = 1; hh < SPL; hh++)
+                        v = h == hh ? e[hh * NU + q][d] : v;
+                    e[q][d] = v;
+                }
+            }
+        }
+        // tiles 4 u0 + t1 are read by all SPL warps of this u0 and rewritten
+        // below
+        GFP_JITTER(3);
+        __syncthreads();
+    }
+    // One balanced normalisation per output, the canonical form on the last
+    // pass; X[u0 + 4 u1] = e[q] goes back to tile 4 u0 + u1 as the source of
+    // its box store.  Output u of group j lives at
+    // (j / Ns) Ns K + (j mod Ns) + u Ns: for Ns >= 32 the warp's 32 groups
+    // are 32 consecutive columns (one {32, k} box, the tile as it is); for
+    // Ns = 16 they are two runs of 16 columns 256 apart (two {16, k} boxes:
+    // the tile holds them as [half][d][16]).
+    __syncwarp();  // Ns = 16 writes other lanes' (already read) columns
+    const bool wide = lNs >= 5;
+    const int ob = wide ? lane : (lane >> 4) * (KD * 16) + (lane & 15);
+    const int os = wide ? 32 : 16;
+#pragma unroll
+    for (int q = 0; q < NU; q++) {
         p44::normalize_el<KD, SPARSE>(e[q], rc);
-        i64 *tile = sm + GFP_IDX((4 * u0 + q) * TILE + lane, K * TILE);
+        i64 *tile = sm + GFP_IDX((4 * u0 + h * NU + q) * TILE + ob, K * TILE);
         if (A.canon) {
             u64 c[KD];
             lazy_to_canonical_bf<KD>(e[q], c, rc);
 #pragma unroll
             for (int d = 0; d < KD; d++)
-                tile[d * 32] = (i64)c[d];
-        } else {
-#pragma unroll
-            for (int d = 0; d < KD; d++)
-                tile[d * 32] = e[q][d];
+                e[q][d] = (i64)c[d];
         }
+#pragma unroll
+        for (int d = 0; d < KD; d++)
+            tile[GFP_IDX(d * os, TILE - ob)] = e[q][d];
     }
     // generic-proxy writes -> async proxy (TMA) reads
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) {
-        // output u of group j at (j / Ns) Ns K + (j mod Ns) + u Ns; Ns >= 32
-        // and j0 % 32 == 0: the warp's 32 groups are 32 consecutive columns
         const int64_t base = (((int64_t)j0 >> lNs) << (lNs + 4)) + (j0 & nsmask);
 #pragma unroll
-        for (int q = 0; q < 4; q++)
-            p44t::tma_store(tout, sm + (4 * u0 + q) * TILE,
-                            (int)(base + ((int64_t)(u0 + 4 * q) << lNs)), bidx, pol);
+        for (int q = 0; q < NU; q++) {
+            const int u1 = h * NU + q;
+            const i64 *tile = sm + (4 * u0 + u1) * TILE;
+            const int c0 = (int)(base + ((int64_t)(u0 + 4 * u1) << lNs));
+            if (wide) {
+                p44t::tma_store(tout, tile, c0, bidx, pol);
+            } else {  // groups j0 + 16 .. j0 + 31 are the next block of Ns K columns
+                p44t::tma_store(tout16, tile, c0, bidx, pol);
+                p44t::tma_store(tout16, tile + KD * 16, c0 + (1 << (lNs + 4)), bidx, pol);
+            }
+        }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         // the tiles must stay until the stores have read them
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -295,14 +339,14 @@ static inline p44t_encode_fn p44t_encoder()
 
 // tensor map of a digit-major vector set: [batch][k][N] u64, box {32, k, 1}
 static inline bool p44t_make_map(CUtensorMap *m, const u64 *base, int64_t N, int k, int64_t batch,
-                                 int64_t batch_stride)
+                                 int64_t batch_stride, int cols = 32)
 {
     p44t_encode_fn enc = p44t_encoder();
     if (!enc || ((uintptr_t)base & 15))
         return false;
     const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)k, (cuuint64_t)batch};
     const cuuint64_t strides[2] = {(cuuint64_t)N * 8, (cuuint64_t)batch_stride * 8};
-    const cuuint32_t box[3] = {32, (cuuint32_t)k, 1};
+    const cuuint32_t box[3] = {(cuuint32_t)cols, (cuuint32_t)k, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, (void *)base, dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -310,12 +354,22 @@ static inline bool p44t_make_map(CUtensorMap *m, const u64 *base, int64_t N, int
            CUDA_SUCCESS;
 }
 
-// the passes k_pass44t takes: a large transform's (grid of at least four
-// waves, the NW = 4 regime of k_pass44) digit-major passes after the first
+// the passes k_pass44t takes: digit-major k = 8 passes after the first
+// (Ns >= 16) of transforms with at least 32 groups
+#ifndef P44T_MIN_CTAS
+#define P44T_MIN_CTAS 0  // smallest grid routed here (A/B builds)
+#endif
 static inline bool p44t_takes(const PassArgs &A, int64_t M, int64_t ctas)
 {
-    return P44_TMA && ctas >= 4 * (int64_t)num_sms() && (M & 31) == 0 && A.lNs >= 5 &&
-           A.lN <= 30 && !A.in_em && !A.out_em && !A.ft_lh && !A.xg && !A.pre && !A.in_canon;
+    return P44_TMA && ctas >= P44T_MIN_CTAS && (M & 31) == 0 && A.lNs >= 4 && A.lN <= 30 &&
+           !A.in_em && !A.out_em && !A.ft_lh && !A.xg && !A.pre && !A.in_canon;
+}
+
+template <int KD, int SP, bool IV>
+static inline void (*p44t_kernel(int nw))(const PassArgs, const PassTma)
+{
+    return nw == 4 ? k_pass44t<KD, SP, IV, 4> : nw == 8 ? k_pass44t<KD, SP, IV, 8>
+                                                        : k_pass44t<KD, SP, IV, 16>;
 }
 
 // returns 1 when the pass was launched
@@ -327,25 +381,33 @@ static int launch_pass44t(const PassArgs &A, int64_t M, int64_t nsets, cudaStrea
     } else {
         PassTma T;
         const int64_t N = (int64_t)1 << A.lN;
-        if (!p44t_make_map(&T.in, A.in, N, KD, A.batch, A.batch_stride) ||
-            !p44t_make_map(&T.out, A.out, N, KD, A.batch, A.batch_stride))
+        const int64_t bs = A.batch_stride;
+        if (!p44t_make_map(&T.in, A.in, N, KD, A.batch, bs) ||
+            !p44t_make_map(&T.out, A.out, N, KD, A.batch, bs) ||
+            !p44t_make_map(&T.out16, A.out, N, KD, A.batch, bs, 16))
             return 0;
         T.in2 = T.in;
         T.out2 = T.out;
-        if (A.in2 && (!p44t_make_map(&T.in2, A.in2, N, KD, A.batch, A.batch_stride) ||
-                      !p44t_make_map(&T.out2, A.out2, N, KD, A.batch, A.batch_stride)))
+        T.out2_16 = T.out16;
+        if (A.in2 && (!p44t_make_map(&T.in2, A.in2, N, KD, A.batch, bs) ||
+                      !p44t_make_map(&T.out2, A.out2, N, KD, A.batch, bs) ||
+                      !p44t_make_map(&T.out2_16, A.out2, N, KD, A.batch, bs, 16)))
             return 0;
+        // elements per thread in phase A as in launch_pass44: 4 when the grid
+        // fills the GPU, fewer (more warps per CTA) for small transforms
+        const int64_t ctas = (M / 32) * nsets;
+        const int nw = ctas >= 4 * (int64_t)num_sms() ? 4 : ctas >= (int64_t)num_sms() ? 8 : 16;
         void (*kern)(const PassArgs, const PassTma) = nullptr;
         const bool inv = A.rot_inv != 0;
         if (A.rc.p3_ok)
-            kern = inv ? k_pass44t<KD, 3, true> : k_pass44t<KD, 3, false>;
+            kern = inv ? p44t_kernel<KD, 3, true>(nw) : p44t_kernel<KD, 3, false>(nw);
         else if (A.rc.p2_ok)
-            kern = inv ? k_pass44t<KD, 2, true> : k_pass44t<KD, 2, false>;
+            kern = inv ? p44t_kernel<KD, 2, true>(nw) : p44t_kernel<KD, 2, false>(nw);
         else
-            kern = inv ? k_pass44t<KD, 0, true> : k_pass44t<KD, 0, false>;
+            kern = inv ? p44t_kernel<KD, 0, true>(nw) : p44t_kernel<KD, 0, false>(nw);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(M / 32), (unsigned)nsets);
-        cfg.blockDim = dim3(128);
+        cfg.blockDim = dim3(nw * 32);
         cfg.dynamicSmemBytes = 0;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
