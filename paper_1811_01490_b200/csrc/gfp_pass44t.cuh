@@ -4,8 +4,8 @@
 // Same pass and the same arithmetic as k_pass44 (gfp_pass44.cuh; the
 // reference's dft_general level, fft.py:298-360, with the level twiddle split
 // r^a omega^b of fft.py:84-103), for the passes that carry the bulk of a large
-// transform: not the first pass (Ns >= 16), digit-major input and output,
-// every group of the CTA present (M % 32 == 0); NW warps per CTA as in
+// transform: digit-major input and output, every group of the CTA present
+// (M % 32 == 0); NW warps per CTA as in
 // k_pass44 (4 for grids that fill the GPU, 8 / 16 for small transforms).  What changes is how the
 // digit rows move:
 //
@@ -182,6 +182,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
 #pragma unroll
         for (int d = 0; d < KD; d++)
             x[d] = tile[((d - tw.as) & (KD - 1)) * 32];
+        if (A.in_canon)  // first pass only, where a = 0
+            to_balanced<KD>(x, rc.r);
         if (mul_tw) {
             const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(
                 A.table_lh + GFP_IDX(tw.b, M) * KD);
@@ -265,6 +267,45 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
         // below
         GFP_JITTER(3);
         __syncthreads();
+    }
+    if (lNs == 0) {
+        // First pass (Ns = 1): output u of group j goes to column 16 j + u, so
+        // the CTA's outputs are 512 consecutive columns of every digit row.
+        // Park them over the tiles as [d][g][u ^ (g mod 16)] (the XOR keeps
+        // both the lane-per-group writes and the lane-per-column reads
+        // conflict-free without padding) and write each row lane-contiguously.
+        constexpr int NT = NW * 32;
+        u64 *out = (blockIdx.y >= A.batch ? A.out2 : A.out) + (int64_t)bidx * A.batch_stride;
+        if (SPL == 1)
+            __syncthreads();  // every warp's stage-2 reads done: the park spans all tiles
+#pragma unroll
+        for (int q = 0; q < NU; q++) {
+            p44::normalize_el<KD, SPARSE>(e[q], rc);
+            if (A.canon) {
+                u64 c[KD];
+                lazy_to_canonical_bf<KD>(e[q], c, rc);
+#pragma unroll
+                for (int d = 0; d < KD; d++)
+                    e[q][d] = (i64)c[d];
+            }
+            const int u = u0 + 4 * (h * NU + q);
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                sm[GFP_IDX(d * 512 + lane * 16 + (u ^ (lane & 15)), K * TILE)] = e[q][d];
+        }
+        GFP_JITTER(4);
+        __syncthreads();
+        u64 *obase = out + ((int64_t)j0 << 4);
+#pragma unroll
+        for (int q4 = 0; q4 < 512 / NT; q4++) {
+            const int c = threadIdx.x + NT * q4;  // column 16 j0 + c
+            const int g = c >> 4, u = c & 15;
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                __stcs(obase + GFP_IDX(((int64_t)d << lN) + c, ((int64_t)KD << lN) - ((int64_t)j0 << 4)),
+                       (u64)sm[GFP_IDX(d * 512 + g * 16 + (u ^ (g & 15)), K * TILE)]);
+        }
+        return;
     }
     // One balanced normalisation per output, the canonical form on the last
     // pass; X[u0 + 4 u1] = e[q] goes back to tile 4 u0 + u1 as the source of
@@ -354,15 +395,19 @@ static inline bool p44t_make_map(CUtensorMap *m, const u64 *base, int64_t N, int
            CUDA_SUCCESS;
 }
 
-// the passes k_pass44t takes: digit-major k = 8 passes after the first
-// (Ns >= 16) of transforms with at least 32 groups
+// the passes k_pass44t takes: the digit-major k = 8 passes of transforms
+// with at least 32 groups (not the pointwise-product, four-step-twiddle,
+// host-memory or fused-exchange forms of the first / last pass)
+#ifndef P44T_FIRST
+#define P44T_FIRST 0  // 0: the first pass (Ns = 1) too; -1: it stays on k_pass44 (A/B builds)
+#endif
 #ifndef P44T_MIN_CTAS
 #define P44T_MIN_CTAS 0  // smallest grid routed here (A/B builds)
 #endif
 static inline bool p44t_takes(const PassArgs &A, int64_t M, int64_t ctas)
 {
-    return P44_TMA && ctas >= P44T_MIN_CTAS && (M & 31) == 0 && A.lNs >= 4 && A.lN <= 30 &&
-           !A.in_em && !A.out_em && !A.ft_lh && !A.xg && !A.pre && !A.in_canon;
+    return P44_TMA && ctas >= P44T_MIN_CTAS && (M & 31) == 0 && (A.lNs >= 4 || A.lNs == P44T_FIRST) &&
+           A.lN <= 30 && !A.in_em && !A.out_em && !A.ft_lh && !A.xg && !A.pre;
 }
 
 template <int KD, int SP, bool IV>
