@@ -300,6 +300,12 @@ int gfp_fft_plan_caps(const gfp_fft_plan *plan);
 int gfp_fft_plan_set_timing(gfp_fft_plan *plan, int on);
 int gfp_fft_plan_pass_times(gfp_fft_plan *plan, float *ms, int *pass, int max);
 
+/* Number of transform pass launches of this process that ran as the TMA form
+   of the k = 8 pass (k_pass44t: cp.async.bulk.tensor tile loads / stores;
+   gfp_pass44t.cuh) -- lets a test or the benchmark confirm which kernel
+   served a transform. */
+int64_t gfp_tma_pass_launches(void);
+
 /* 1 in the checked build (GFP_DEBUG: index guards + timing jitter in the
    pass / exchange kernels, the stand-in for compute-sanitizer), else 0.
    gfp_debug_selftest launches one kernel that performs a deliberately

@@ -55,6 +55,9 @@ inline void once_per_device(unsigned long long &mask, F &&f)
 
 struct gfp_fft_plan;
 
+// pass launches served by k_pass44t (gfp_tma_pass_launches)
+extern long long g_tma_pass_launches;
+
 #define GFP_MAX_GRID_Y 65535  // pass kernels put the batch in grid.y
 #define GFP_MAX_TIMED 64  // pass launches timed per call (gfp_fft_plan_pass_times)
 

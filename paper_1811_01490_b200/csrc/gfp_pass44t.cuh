@@ -41,8 +41,8 @@
 
 // tensor maps of one pass launch: the two vector sets' inputs and outputs
 struct PassTma {
-    CUtensorMap in, in2, out, out2;  // box {32, k, 1}
-    CUtensorMap out16, out2_16;      // box {16, k, 1}: the stores of the Ns = 16 pass
+    CUtensorMap in, in2;    // box {32, k, 1}
+    CUtensorMap out, out2;  // box {32, k, 1}; {16, k, 1} for the Ns = 16 pass
 };
 
 namespace p44t {
@@ -75,6 +75,18 @@ GFP_D void mbar_wait(u64 *bar, unsigned parity)
         "}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+}
+GFP_D bool elect_one()
+{
+    unsigned pred;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}"
+        : "=r"(pred));
+    return pred != 0;
 }
 GFP_D u64 evict_first_policy()
 {
@@ -127,15 +139,17 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
     __shared__ __align__(128) i64 sm[K * TILE];
     __shared__ __align__(8) u64 bar[K];
     const int lane = threadIdx.x & 31;
-    const int w = threadIdx.x >> 5;  // elements t = w + NW i
+    // elements t = w + NW i; broadcast so the compiler keeps w (and the TMA
+    // operands derived from it) in uniform registers
+    const int w = __shfl_sync(FULL_MASK, threadIdx.x >> 5, 0);
+    const bool leader = p44t::elect_one();  // one lane issues the warp's TMA operations
 
     int bidx = blockIdx.y;
-    const CUtensorMap *tin = &T.in, *tout = &T.out, *tout16 = &T.out16;
+    const CUtensorMap *tin = &T.in, *tout = &T.out;
     if (bidx >= A.batch) {
         bidx -= (int)A.batch;
         tin = &T.in2;
         tout = &T.out2;
-        tout16 = &T.out2_16;
     }
     const int lN = A.lN, lM = A.lM, lNs = A.lNs;
     const int64_t N = (int64_t)1 << lN, M = (int64_t)1 << lM;
@@ -156,7 +170,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const u64 pol = p44t::evict_first_policy();
-    if (lane == 0) {
+    if (leader) {
 #pragma unroll
         for (int i = 0; i < EPT; i++) {
             const int t = w + NW * i;
@@ -173,8 +187,34 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
     for (int i = 0; i < EPT; i++) {
         const int t = w + NW * i;
         i64 *tile = sm + GFP_IDX(t * TILE + lane, K * TILE);
-        const p44::Twiddle tw =
-            p44::twiddle_of<KD>(t, j, nsmask, lM, lNs, N, M, A.neg_exp, A.root_inv);
+        // omega^E = r^a omega^b, E = t (j mod Ns)(M / Ns) < N <= 2^30: 32-bit
+        // arithmetic; the first pass of a four-step row transform carries the
+        // enclosing transform's twiddle w^(+-(row0 + b) pos) instead (its own
+        // is trivial)
+        unsigned E = ((unsigned)t * ((unsigned)j & (unsigned)nsmask)) << (lM - lNs);
+        if (A.neg_exp && E)
+            E = (unsigned)N - E;
+        int tlM = lM, troot_inv = A.root_inv;
+        const u64 *tab = A.table_lh;
+        if (A.ft_lh) {
+            const int64_t Nf = (int64_t)1 << A.ft_lN;
+            int64_t Ef = ((A.ft_row0 + bidx) * (j + ((int64_t)t << lM))) & (Nf - 1);
+            if (A.ft_inv && Ef)
+                Ef = Nf - Ef;
+            E = (unsigned)Ef;
+            tlM = A.ft_lM;
+            troot_inv = A.ft_root_inv;
+            tab = A.ft_lh;
+        }
+        p44::Twiddle tw;
+        {
+            int a = (int)(E >> tlM);
+            tw.b = E & ((1u << tlM) - 1u);
+            if (troot_inv && a)
+                a = 2 * KD - a;
+            tw.as = a & (KD - 1);
+            tw.negx = ((1u << tw.as) - 1u) ^ (a >= KD ? ((1u << KD) - 1u) : 0u);
+        }
         // warp-uniform multiply: lanes with b = 0 multiply by table[0] = 1
         const bool mul_tw = __any_sync(FULL_MASK, tw.b || A.scale);
         p44t::mbar_wait(&bar[t], 0);
@@ -186,7 +226,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
             to_balanced<KD>(x, rc.r);
         if (mul_tw) {
             const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(
-                A.table_lh + GFP_IDX(tw.b, M) * KD);
+                tab + GFP_IDX(tw.b, (int64_t)1 << tlM) * KD);
             u64 ylh[KD];
 #pragma unroll
             for (int d = 0; d < KD; d += 2) {
@@ -336,7 +376,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
     // generic-proxy writes -> async proxy (TMA) reads
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
-    if (lane == 0) {
+    if (leader) {
         const int64_t base = (((int64_t)j0 >> lNs) << (lNs + 4)) + (j0 & nsmask);
 #pragma unroll
         for (int q = 0; q < NU; q++) {
@@ -346,8 +386,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
             if (wide) {
                 p44t::tma_store(tout, tile, c0, bidx, pol);
             } else {  // groups j0 + 16 .. j0 + 31 are the next block of Ns K columns
-                p44t::tma_store(tout16, tile, c0, bidx, pol);
-                p44t::tma_store(tout16, tile + KD * 16, c0 + (1 << (lNs + 4)), bidx, pol);
+                p44t::tma_store(tout, tile, c0, bidx, pol);
+                p44t::tma_store(tout, tile + KD * 16, c0 + (1 << (lNs + 4)), bidx, pol);
             }
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -378,8 +418,8 @@ static inline p44t_encode_fn p44t_encoder()
     return fn;
 }
 
-// tensor map of a digit-major vector set: [batch][k][N] u64, box {32, k, 1}
-static inline bool p44t_make_map(CUtensorMap *m, const u64 *base, int64_t N, int k, int64_t batch,
+// tensor map of a digit-major vector set: [batch][k][N] u64, box {cols, k, 1}
+static inline bool p44t_encode_map(CUtensorMap *m, const u64 *base, int64_t N, int k, int64_t batch,
                                  int64_t batch_stride, int cols = 32)
 {
     p44t_encode_fn enc = p44t_encoder();
@@ -395,9 +435,48 @@ static inline bool p44t_make_map(CUtensorMap *m, const u64 *base, int64_t N, int
            CUDA_SUCCESS;
 }
 
+// The same through a small per-thread cache: a descriptor depends only on the
+// base address and the shape, and a transform's passes alternate between a
+// few buffers, so repeated calls (C1 / C2 are launch-bound when launched
+// from a stream) encode nothing.
+static inline bool p44t_make_map(CUtensorMap *m, const u64 *base, int64_t N, int k, int64_t batch,
+                                 int64_t batch_stride, int cols = 32)
+{
+    struct Entry {
+        const u64 *base;
+        int64_t N, batch, stride;
+        int k, cols, valid;
+        CUtensorMap map;
+    };
+    constexpr int NE = 32;
+    static thread_local Entry cache[NE];
+    static thread_local int next = 0;
+    for (int i = 0; i < NE; i++) {
+        const Entry &c = cache[i];
+        if (c.valid && c.base == base && c.N == N && c.batch == batch && c.stride == batch_stride &&
+            c.k == k && c.cols == cols) {
+            *m = c.map;
+            return true;
+        }
+    }
+    if (!p44t_encode_map(m, base, N, k, batch, batch_stride, cols))
+        return false;
+    Entry &c = cache[next];
+    next = (next + 1) % NE;
+    c.base = base;
+    c.N = N;
+    c.batch = batch;
+    c.stride = batch_stride;
+    c.k = k;
+    c.cols = cols;
+    c.map = *m;
+    c.valid = 1;
+    return true;
+}
+
 // the passes k_pass44t takes: the digit-major k = 8 passes of transforms
-// with at least 32 groups (not the pointwise-product, four-step-twiddle,
-// host-memory or fused-exchange forms of the first / last pass)
+// with at least 32 groups (not the pointwise-product, host-memory or
+// fused-exchange forms of the first / last pass)
 #ifndef P44T_FIRST
 #define P44T_FIRST 0  // 0: the first pass (Ns = 1) too; -1: it stays on k_pass44 (A/B builds)
 #endif
@@ -407,7 +486,7 @@ static inline bool p44t_make_map(CUtensorMap *m, const u64 *base, int64_t N, int
 static inline bool p44t_takes(const PassArgs &A, int64_t M, int64_t ctas)
 {
     return P44_TMA && ctas >= P44T_MIN_CTAS && (M & 31) == 0 && (A.lNs >= 4 || A.lNs == P44T_FIRST) &&
-           A.lN <= 30 && !A.in_em && !A.out_em && !A.ft_lh && !A.xg && !A.pre;
+           A.lN <= 30 && A.ft_lN <= 30 && !A.in_em && !A.out_em && !A.xg && !A.pre;
 }
 
 template <int KD, int SP, bool IV>
@@ -427,16 +506,16 @@ static int launch_pass44t(const PassArgs &A, int64_t M, int64_t nsets, cudaStrea
         PassTma T;
         const int64_t N = (int64_t)1 << A.lN;
         const int64_t bs = A.batch_stride;
+        // the stores are {32, k} boxes for Ns >= 32, {16, k} boxes for Ns = 16
+        // (and plain row stores in the first pass)
+        const int ocols = A.lNs == 4 ? 16 : 32;
         if (!p44t_make_map(&T.in, A.in, N, KD, A.batch, bs) ||
-            !p44t_make_map(&T.out, A.out, N, KD, A.batch, bs) ||
-            !p44t_make_map(&T.out16, A.out, N, KD, A.batch, bs, 16))
+            !p44t_make_map(&T.out, A.out, N, KD, A.batch, bs, ocols))
             return 0;
         T.in2 = T.in;
         T.out2 = T.out;
-        T.out2_16 = T.out16;
         if (A.in2 && (!p44t_make_map(&T.in2, A.in2, N, KD, A.batch, bs) ||
-                      !p44t_make_map(&T.out2, A.out2, N, KD, A.batch, bs) ||
-                      !p44t_make_map(&T.out2_16, A.out2, N, KD, A.batch, bs, 16)))
+                      !p44t_make_map(&T.out2, A.out2, N, KD, A.batch, bs, ocols)))
             return 0;
         // elements per thread in phase A as in launch_pass44: 4 when the grid
         // fills the GPU, fewer (more warps per CTA) for small transforms
@@ -461,6 +540,7 @@ static int launch_pass44t(const PassArgs &A, int64_t M, int64_t nsets, cudaStrea
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         cudaLaunchKernelEx(&cfg, kern, A, T);
+        __atomic_fetch_add(&g_tma_pass_launches, 1, __ATOMIC_RELAXED);
         return 1;
     }
 }

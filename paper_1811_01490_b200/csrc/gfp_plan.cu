@@ -496,6 +496,9 @@ int64_t gfp_fft_workspace_words(const gfp_fft_plan *p, int64_t batch)
 
 int64_t gfp_fft_plan_last_launches(const gfp_fft_plan *p) { return p ? p->last_launches : 0; }
 
+long long g_tma_pass_launches = 0;
+int64_t gfp_tma_pass_launches(void) { return __atomic_load_n(&g_tma_pass_launches, __ATOMIC_RELAXED); }
+
 int gfp_fft_plan_caps(const gfp_fft_plan *p)
 {
     if (!p || !em_io_supported(p))
