@@ -35,6 +35,13 @@
 #ifndef P44T_MINB
 #define P44T_MINB 5  // CTAs per SM the kernel is register-bounded for (32 KB tiles each)
 #endif
+#ifndef P44T_EARLY_TABLE_MINEPT
+#define P44T_EARLY_TABLE_MINEPT 4  // elements per thread from which the table entry is loaded
+                                   // before the tile wait
+#endif
+#ifndef P44T_UNROLL_A_MAXEPT
+#define P44T_UNROLL_A_MAXEPT 0  // phase-A loop unrolled up to this many elements per thread
+#endif
 #ifndef P44T_EVICT_FIRST
 #define P44T_EVICT_FIRST 1  // streamed tiles carry an L2 evict-first policy (tables stay)
 #endif
@@ -183,7 +190,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
     // r^a omega^b; r^a is the row the digit is read from (and a sign folded
     // into the multiply's limb split), omega^b one general multiply whose
     // digits go back to the tile as they become final
-#pragma unroll 1
+    constexpr int UNR_A = EPT <= P44T_UNROLL_A_MAXEPT ? EPT : 1;
+#pragma unroll UNR_A
     for (int i = 0; i < EPT; i++) {
         const int t = w + NW * i;
         i64 *tile = sm + GFP_IDX(t * TILE + lane, K * TILE);
@@ -217,6 +225,23 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
         }
         // warp-uniform multiply: lanes with b = 0 multiply by table[0] = 1
         const bool mul_tw = __any_sync(FULL_MASK, tw.b || A.scale);
+        // With four elements per thread (large transforms) the table entry is
+        // requested before the wait for the tile, so the two latencies overlap
+        // (C4 passes 0.718 -> 0.708 ms); with one or two (C1 / C2) the sixteen
+        // registers held across the wait cost more than the overlap gains
+        // (C2 graph 0.0717 -> 0.0737 ms), so those load it after the wait.
+        constexpr bool EARLY = EPT >= P44T_EARLY_TABLE_MINEPT;
+        u64 ylh[KD];
+        const ulonglong2 *tp =
+            reinterpret_cast<const ulonglong2 *>(tab + GFP_IDX(tw.b, (int64_t)1 << tlM) * KD);
+        if (EARLY && mul_tw) {
+#pragma unroll
+            for (int d = 0; d < KD; d += 2) {
+                const ulonglong2 v = __ldg(tp + d / 2);
+                ylh[d] = v.x;
+                ylh[d + 1] = v.y;
+            }
+        }
         p44t::mbar_wait(&bar[t], 0);
         i64 x[KD], f[KD];
 #pragma unroll
@@ -225,14 +250,13 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
         if (A.in_canon)  // first pass only, where a = 0
             to_balanced<KD>(x, rc.r);
         if (mul_tw) {
-            const ulonglong2 *tp = reinterpret_cast<const ulonglong2 *>(
-                tab + GFP_IDX(tw.b, (int64_t)1 << tlM) * KD);
-            u64 ylh[KD];
+            if (!EARLY) {
 #pragma unroll
-            for (int d = 0; d < KD; d += 2) {
-                const ulonglong2 v = __ldg(tp + d / 2);
-                ylh[d] = v.x;
-                ylh[d + 1] = v.y;
+                for (int d = 0; d < KD; d += 2) {
+                    const ulonglong2 v = __ldg(tp + d / 2);
+                    ylh[d] = v.x;
+                    ylh[d + 1] = v.y;
+                }
             }
             fast_mul_lazy_ylimbs<KD, SPARSE, true, 32>(x, ylh, f, rc, tw.negx, tile);
         } else {  // r^a alone (t = 0: the identity)
