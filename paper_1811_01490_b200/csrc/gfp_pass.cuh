@@ -174,23 +174,32 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
         int64_t b = 0;
         unsigned negx = 0;
         if (active) {
-            // E = t (j mod Ns) (M / Ns) < N; omega^E = (omega^M)^a omega^b
-            int64_t E = ((int64_t)t * (j & nsmask)) << (lM - lNs);
-            if (A.neg_exp && E)
-                E = N - E;
-            int a = (int)(E >> lM);
-            b = E & (M - 1);
-            // omega^M is r (or 1/r for plans built on an inverse root)
-            if (A.root_inv && a)
-                a = 2 * KD - a;
-            const int as = a & (KD - 1);
-            negx = (unsigned)(((1ull << as) - 1ull) ^ (a >= KD ? ((1ull << KD) - 1ull) : 0ull));
             const u64 *src = in + pos;
             const unsigned rowN = 1u << lN;
+            if constexpr (NOMUL) {
+                // first pass (Ns = 1): E = 0, no rotation, no sign -- plain
+                // digit-row loads (streamed once: evict-first)
 #pragma unroll
-            for (int d = 0; d < KD; d++)
-                x[d] = (i64)__ldg(src + GFP_IDX((size_t)((unsigned)((d - as) & (KD - 1)) * rowN),
-                                                (int64_t)KD * N - pos));
+                for (int d = 0; d < KD; d++)
+                    x[d] = (i64)__ldcs(src + GFP_IDX((size_t)d * rowN, (int64_t)KD * N - pos));
+            } else {
+                // E = t (j mod Ns) (M / Ns) < N; omega^E = (omega^M)^a omega^b
+                int64_t E = ((int64_t)t * (j & nsmask)) << (lM - lNs);
+                if (A.neg_exp && E)
+                    E = N - E;
+                int a = (int)(E >> lM);
+                b = E & (M - 1);
+                // omega^M is r (or 1/r for plans built on an inverse root)
+                if (A.root_inv && a)
+                    a = 2 * KD - a;
+                const int as = a & (KD - 1);
+                negx = (unsigned)(((1ull << as) - 1ull) ^
+                                  (a >= KD ? ((1ull << KD) - 1ull) : 0ull));
+#pragma unroll
+                for (int d = 0; d < KD; d++)
+                    x[d] = (i64)__ldg(src + GFP_IDX((size_t)((unsigned)((d - as) & (KD - 1)) * rowN),
+                                                    (int64_t)KD * N - pos));
+            }
             if (A.in_canon)  // pass 0 only, where a = 0
                 to_balanced<KD>(x, rc.r);
             if (!NOMUL && pre) {  // pass 0 only (a = b = 0)
@@ -264,6 +273,10 @@ __global__ void __launch_bounds__(KD >= 16 ? 128 : 256,
                 for (int d = 0; d < KD; d++)
                     row[d] = 0;
             }
+        } else if (NOMUL) {
+#pragma unroll
+            for (int d = 0; d < KD; d++)
+                row[d] = x[d];
         } else {
 #pragma unroll
             for (int d = 0; d < KD; d++)
