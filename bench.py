@@ -842,6 +842,20 @@ def extra_configs(args, dev, flush, stream, hbm_peak, imad_peak):
                 t = timed_loop(step, steps, 2, 1, flush, stream)
                 ms = sum(t) / len(t)
                 entry.update(ms_fwd_plus_inv=ms, elements_per_s=N / (ms * 1e-3))
+                # the same six pass launches replayed from a CUDA graph (as the
+                # C2 headline is): stream-launched, C1 is bound by launch latency
+                graph = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream()
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    step()
+                    with torch.cuda.graph(graph, stream=side):
+                        step()
+                torch.cuda.current_stream().wait_stream(side)
+                torch.cuda.synchronize()
+                t = timed_loop(graph.replay, steps, 2, 1, flush, stream)
+                entry["ms_fwd_plus_inv_graph"] = sum(t) / len(t)
+                del graph
                 xh, keep = _pinned_em(gp, x)
 
                 def e2e():

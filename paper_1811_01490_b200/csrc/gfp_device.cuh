@@ -476,30 +476,28 @@ GFP_D void lazy_to_canonical_bf(const i64 (&f)[KD], u64 (&z)[KD], const RadixCon
         g |= (Mask)(f[i] < 0) << i;
         p |= (Mask)(f[i] == 0) << i;
     }
+    // A borrow out of the top digit means the value D is negative and the
+    // canonical residue is D + p = (D + 1) + r^k: add the 1 to digit 0 first
+    // (still |f_0 + 1| < r) and run the lookahead on the adjusted masks, so the
+    // digits below are final -- no carry loop through r - 1 digits afterwards.
+    const Mask gp0 = g | p;
+    const Mask neg = (((gp0 + g) ^ gp0 ^ g) >> KD) & 1u;
+    const i64 f0 = f[0] + (i64)neg;
+    g = (g & ~(Mask)1) | (Mask)(f0 < 0);
+    p = (p & ~(Mask)1) | (Mask)(f0 == 0);
     const Mask gp = g | p;
     const Mask b = (gp + g) ^ gp ^ g;  // bit i: borrow into digit i (bit k: out of the top)
 #pragma unroll
     for (int i = 0; i < KD; i++) {
-        const i64 t = f[i] - (i64)((b >> i) & 1u);
+        const i64 t = (i ? f[i] : f0) - (i64)((b >> i) & 1u);
         z[i] = (u64)(((b >> (i + 1)) & 1u) ? t + (i64)rc.r : t);
     }
-    // a borrow out of the top digit: value = Z + 1 (r^k = -1), carried
-    // through r - 1 digits; carrying out of the top means p - 1 (form B)
-    if ((b >> KD) & 1u) {
-        bool ca = true;
+    // D = -1: D + 1 = 0 has no borrow left; the residue is p - 1 = r^k (form B)
+    if (neg && !((b >> KD) & 1u)) {
 #pragma unroll
-        for (int i = 0; i < KD; i++) {
-            const u64 v = z[i];
-            const bool zt = v == rc.r - 1;
-            z[i] = ca ? (zt ? 0 : v + 1) : v;
-            ca = ca && zt;
-        }
-        if (ca) {
-#pragma unroll
-            for (int i = 0; i < KD - 1; i++)
-                z[i] = 0;
-            z[KD - 1] = rc.r;
-        }
+        for (int i = 0; i < KD - 1; i++)
+            z[i] = 0;
+        z[KD - 1] = rc.r;
     }
 }
 #else

@@ -12,6 +12,7 @@
 #include "gfp_fast.cuh"
 #include "gfp_pass44.cuh"
 #include "gfp_pass44t.cuh"
+#include "gfp_pass16t.cuh"
 
 // k values whose pass multiply keeps the twiddle limbs in shared memory
 // (fast_mul_window_store) instead of registers
@@ -537,6 +538,10 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
         return cuda_status();
     if (A.in_em || A.out_em || A.ft_lh || A.xg)
         return GFP_EUNSUPPORTED;
+    if constexpr (KD == 16) {  // the multiply-free first pass on TMA tiles
+        if (p16t_takes(A, p->M) && launch_first16t(A, p->M, in2 ? 2 * batch : batch, st))
+            return cuda_status();
+    }
     dim3 grid((unsigned)((p->M + G - 1) / G), (unsigned)(in2 ? 2 * batch : batch));
     if constexpr (P2Radix<KD>::a != 0) {
         if (p->rc.p3_ok) {
