@@ -339,9 +339,19 @@ def pass_roofline(gp, plan, fn, k, N, K, batch, kind, hbm_peak, imad_peak, reps=
     runs = [F.pass_times(plan, fn)[1] for _ in range(reps)]
     e = passes(N, K)
     out = []
+    fused_mid = kind == "polymul" and len(runs[0]) == 2 * e - 1
     for i, (p, _) in enumerate(runs[0]):
         ms = statistics.median(r[i][1] for r in runs)
-        if kind == "polymul":
+        fused = False
+        if fused_mid:
+            # 2e - 1 launches: forward passes 0 .. e-2 (both operands), ONE
+            # kernel for the forward last pass + pointwise product + inverse
+            # first pass (k_pmid44t), inverse passes 1 .. e-1
+            fused = i == e - 1
+            inverse, sets, pre = i >= e, (2 if i < e - 1 else 1), False
+            if i >= e:
+                p = i - e + 1
+        elif kind == "polymul":
             inverse, first_inv = i >= e, i == e
             sets = 2 if i < e else 1
             pre = first_inv
@@ -350,10 +360,15 @@ def pass_roofline(gp, plan, fn, k, N, K, batch, kind, hbm_peak, imad_peak, reps=
         elems = batch * sets * N
         nbytes = elems * 2 * 8 * k + (batch * N * 8 * k if pre else 0)
         mults = batch * sets * mults_in_pass(N, K, p, inverse, pre)
+        if fused:  # reads both operands, writes one vector
+            nbytes = batch * N * 3 * 8 * k
+            mults = batch * (2 * mults_in_pass(N, K, e - 1, False, False) +
+                             mults_in_pass(N, K, 0, True, True))
         imad = mults * 4 * k * k
         gbs = nbytes / (ms * 1e-3) / 1e9
         timad = imad / (ms * 1e-3)
-        entry = {"launch": i, "pass": p, "inverse": inverse, "ms": ms, "hbm_bytes": nbytes,
+        entry = {"launch": i, "pass": "fwd%d+mul+inv0" % (e - 1) if fused else p,
+                 "inverse": inverse, "ms": ms, "hbm_bytes": nbytes,
                  "gbs": gbs, "hbm_frac": gbs / hbm_peak, "general_mults": mults,
                  "tera_imad_per_s": timad / 1e12, "imad_frac": timad / imad_peak,
                  "bound": "hbm" if mults == 0 else "int"}
@@ -550,9 +565,9 @@ def run_ours(args, ws, rank, local):
                    "l2": "256 MiB buffer written between timed steps (inputs fit in L2)",
                    "graph": "CUDA graph of the %d pass kernels per step" % launches_per_step},
         "roofline": {"bound": "int",
-                     "kernel": "k_pass44t<8> / k_pass44<8> (the %d pass launches of the step: 7 "
-                               "TMA-tile passes, the pointwise-product pass on k_pass44)"
-                               % launches_per_step,
+                     "kernel": "k_pass44t<8> / k_pmid44t<8> (the %d launches of the step: the "
+                               "TMA-tile passes and the fused forward-last + pointwise + "
+                               "inverse-first kernel)" % launches_per_step,
                      "achieved": achieved / 1e12, "peak": peak_imad / 1e12,
                      "unit": "T IMAD.WIDE/s", "frac": achieved / peak_imad,
                      "executed": {"achieved": executed / 1e12, "frac": executed / peak_imad,

@@ -171,6 +171,14 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2, 
                 int in_canon, const PassIO *em, cudaStream_t st);
 
 
+// The middle of a k = 8 poly-multiply as one kernel (gfp_pmid44t.cuh): the
+// forward last pass of both operands, the pointwise product and the inverse
+// first pass.  f_in / g_in: the operands after the forward passes 0 .. e-2;
+// out: the inverse's first-pass output (balanced lazy digits).
+bool poly_mid_supported(const gfp_fft_plan *p);
+int launch_poly_mid(const gfp_fft_plan *p, const u64 *f_in, const u64 *g_in, u64 *out,
+                    int64_t batch, cudaStream_t st);
+
 #define DISPATCH_K(k, CALL)                                                                     \
     switch (k) {                                                                                \
     case 1: { constexpr int KD = 1; CALL; } break;                                              \

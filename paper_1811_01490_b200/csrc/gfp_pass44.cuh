@@ -28,6 +28,12 @@
 // K = 16 = 4 x 4 needs 4 lazy radix-2 stages without normalisation; the
 // launcher only selects this kernel when the host bound check allows it
 // (RadixConsts::stages_per_norm >= 4).
+//
+// Since round 2 the digit-major passes of transforms with >= 32 groups run as
+// k_pass44t (gfp_pass44t.cuh: the same pass on TMA tiles).  This kernel keeps
+// what that one does not take: the pointwise-product pass of a poly-multiply,
+// the element-major (host-memory) first / last passes, the fused four-step
+// exchange, and transforms under 512 points.
 #pragma once
 #include "gfp_internal.cuh"
 #include "gfp_fast.cuh"

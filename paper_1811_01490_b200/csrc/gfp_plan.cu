@@ -588,6 +588,63 @@ int gfp_fft_exec_exchange(const gfp_fft_plan *cp, const uint64_t *in, uint64_t *
                          out_canon ? 1 : 0, (cudaStream_t)stream, &io);
 }
 
+// poly-multiply with the fused middle kernel: buffers o (the result), G,
+// scratch, scratch_b hold `nb` vectors each; f and g are never written
+static int poly_mul_fused(gfp_fft_plan *p, const u64 *f, const u64 *g, u64 *o, u64 *G, u64 *scratch,
+                          u64 *scratch_b, int64_t nb, cudaStream_t st)
+{
+    const int e = p->e;
+    const u64 *sf = f, *sg = g;
+    u64 *bf[2] = {o, scratch}, *bg[2] = {G, scratch_b};
+    int64_t Ns = 1;
+    int rcode = GFP_OK;
+    for (int pass = 0; pass + 1 < e; pass++) {  // forward passes 0 .. e-2
+        u64 *df = bf[pass & 1] == sf ? bf[(pass & 1) ^ 1] : bf[pass & 1];
+        u64 *dg = bg[pass & 1] == sg ? bg[(pass & 1) ^ 1] : bg[pass & 1];
+        timing_mark(p, st, -1);
+        rcode = launch_pass<8>(p, sf, df, sg, dg, nullptr, nb, Ns, 0, 0, 0, pass == 0, nullptr, st);
+        if (rcode)
+            return rcode;
+        timing_mark(p, st, pass);
+        p->last_launches++;
+        sf = df;
+        sg = dg;
+        Ns *= p->K;
+    }
+    // fused middle: (sf, sg) -> the buffer of {o, scratch} that is not sf,
+    // chosen so that the inverse's remaining e - 1 passes end in o
+    // (ping-pong: the last launch must land in o)
+    const int rem = e - 1;  // inverse launches after the fused one
+    u64 *dm = (rem % 2 == 0) ? o : scratch;
+    if (dm == sf)  // (e.g. e = 2: the forward pass 0 wrote o): use the other and copy at the end
+        dm = dm == o ? scratch : o;
+    timing_mark(p, st, -1);
+    rcode = launch_poly_mid(p, sf, sg, dm, nb, st);
+    if (rcode)
+        return rcode;
+    timing_mark(p, st, e - 1);
+    p->last_launches++;
+    const u64 *src = dm;
+    Ns = p->K;
+    for (int pass = 1; pass < e; pass++) {  // inverse passes 1 .. e-1
+        u64 *dst = src == o ? scratch : o;
+        const int last = pass + 1 == e;
+        timing_mark(p, st, -1);
+        rcode = launch_pass<8>(p, src, dst, nullptr, nullptr, nullptr, nb, Ns, 1, last, last, 0,
+                               nullptr, st);
+        if (rcode)
+            return rcode;
+        timing_mark(p, st, pass);
+        p->last_launches++;
+        src = dst;
+        Ns *= p->K;
+    }
+    if (src != o)
+        cudaMemcpyAsync(o, src, sizeof(u64) * (size_t)p->k * p->N * nb, cudaMemcpyDeviceToDevice,
+                        st);
+    return cuda_status();
+}
+
 int gfp_poly_mul(const gfp_fft_plan *cp, const uint64_t *f, const uint64_t *g, uint64_t *out,
                  uint64_t *work, int64_t batch, void *stream)
 {
@@ -613,6 +670,12 @@ int gfp_poly_mul(const gfp_fft_plan *cp, const uint64_t *f, const uint64_t *g, u
             err = run_generic(p, f + b0 * ew, o, scratch, nb, 0, st);
             if (!err)
                 err = run_generic(p, g + b0 * ew, G, scratch_b, nb, 0, st);
+        } else if (poly_mid_supported(p)) {
+            // forward passes 0 .. e-2 of both operands, then ONE kernel for the
+            // forward last pass + pointwise product + inverse first pass, then
+            // the inverse passes 1 .. e-1 (2 e - 1 launches instead of 2 e)
+            err = poly_mul_fused(p, f + b0 * ew, g + b0 * ew, o, G, scratch, scratch_b, nb, st);
+            continue;
         } else {
             err = run_transform2(p, f + b0 * ew, o, scratch, g + b0 * ew, G, scratch_b, nullptr,
                                  nb, 0, 1, 0, st);
