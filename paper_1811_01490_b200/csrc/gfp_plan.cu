@@ -591,7 +591,8 @@ int gfp_fft_exec_exchange(const gfp_fft_plan *cp, const uint64_t *in, uint64_t *
 // poly-multiply with the fused middle kernel: buffers o (the result), G,
 // scratch, scratch_b hold `nb` vectors each; f and g are never written
 static int poly_mul_fused(gfp_fft_plan *p, const u64 *f, const u64 *g, u64 *o, u64 *G, u64 *scratch,
-                          u64 *scratch_b, int64_t nb, cudaStream_t st)
+                          u64 *scratch_b, int64_t nb, cudaStream_t st,
+                          const PassIO *em_fwd = nullptr, const PassIO *em_inv = nullptr)
 {
     const int e = p->e;
     const u64 *sf = f, *sg = g;
@@ -602,7 +603,7 @@ static int poly_mul_fused(gfp_fft_plan *p, const u64 *f, const u64 *g, u64 *o, u
         u64 *df = bf[pass & 1] == sf ? bf[(pass & 1) ^ 1] : bf[pass & 1];
         u64 *dg = bg[pass & 1] == sg ? bg[(pass & 1) ^ 1] : bg[pass & 1];
         timing_mark(p, st, -1);
-        rcode = launch_pass<8>(p, sf, df, sg, dg, nullptr, nb, Ns, 0, 0, 0, pass == 0, nullptr, st);
+        rcode = launch_pass<8>(p, sf, df, sg, dg, nullptr, nb, Ns, 0, 0, 0, pass == 0, em_fwd, st);
         if (rcode)
             return rcode;
         timing_mark(p, st, pass);
@@ -631,7 +632,7 @@ static int poly_mul_fused(gfp_fft_plan *p, const u64 *f, const u64 *g, u64 *o, u
         const int last = pass + 1 == e;
         timing_mark(p, st, -1);
         rcode = launch_pass<8>(p, src, dst, nullptr, nullptr, nullptr, nb, Ns, 1, last, last, 0,
-                               nullptr, st);
+                               em_inv, st);
         if (rcode)
             return rcode;
         timing_mark(p, st, pass);
@@ -639,6 +640,8 @@ static int poly_mul_fused(gfp_fft_plan *p, const u64 *f, const u64 *g, u64 *o, u
         src = dst;
         Ns *= p->K;
     }
+    if (em_inv && em_inv->out)
+        return cuda_status();  // the last pass wrote the element-major output
     if (src != o)
         cudaMemcpyAsync(o, src, sizeof(u64) * (size_t)p->k * p->N * nb, cudaMemcpyDeviceToDevice,
                         st);
@@ -792,12 +795,16 @@ int gfp_poly_mul_host2(gfp_fft_plan *p, const uint64_t *f, int64_t nf, const uin
     // forward transforms of both operands in the same launches; pass 0 reads
     // the element-major operands (zero past nf / ng); spectra stay lazy
     PassIO e1 = {mf, mg, nf, ng, nullptr, 0, nullptr, 0, 0};
-    err = run_transform2(p, F, F, s1, G, G, s2, nullptr, batch, 0, 1, 0, st, &e1);
-    if (!err) {
-        // inverse of F .* G (pointwise product fused into pass 0, N^-1 into
-        // the last pass), which writes the first n_out elements element-major
-        PassIO e2 = {nullptr, nullptr, 0, 0, dout, n_out, nullptr, 0, 0};
-        err = run_transform(p, F, F, s1, G, batch, 1, 0, 1, st, &e2);
+    PassIO e2 = {nullptr, nullptr, 0, 0, dout, n_out, nullptr, 0, 0};
+    if (poly_mid_supported(p)) {  // the middle as one kernel (gfp_pmid44t.cuh)
+        err = poly_mul_fused(p, F, G, F, G, s1, s2, batch, st, &e1, &e2);
+    } else {
+        err = run_transform2(p, F, F, s1, G, G, s2, nullptr, batch, 0, 1, 0, st, &e1);
+        if (!err) {
+            // inverse of F .* G (pointwise product fused into pass 0, N^-1 into
+            // the last pass), which writes the first n_out elements element-major
+            err = run_transform(p, F, F, s1, G, batch, 1, 0, 1, st, &e2);
+        }
     }
     if (!err && !mo) {
         cudaMemcpyAsync(out, dout, sizeof(u64) * k * n_out * batch, cudaMemcpyDeviceToHost, st);

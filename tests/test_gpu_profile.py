@@ -97,9 +97,9 @@ def test_pass_times_and_caps(cuda):
     assert [i for i, _ in passes] == [0, 1, 2, 3] and all(ms > 0 for _, ms in passes)
     _, passes = F.pass_times(plan, lambda: gp.poly_mul(x, x, plan))
     # forward passes 0-2 (both operands), the fused forward-last + pointwise
-        # + inverse-first kernel (marked with the forward pass index 3), inverse
-        # passes 1-3
-        assert [i for i, _ in passes] == [0, 1, 2, 3, 1, 2, 3]
+    # + inverse-first kernel (marked with the forward pass index 3), inverse
+    # passes 1-3
+    assert [i for i, _ in passes] == [0, 1, 2, 3, 1, 2, 3]
     # timing off again: no marks recorded
     gp.fft_tensor(x, plan)
     assert lib.gfp_fft_plan_pass_times(plan.handle, None, None, 0) == 0
