@@ -300,9 +300,11 @@ int gfp_fft_plan_caps(const gfp_fft_plan *plan);
 int gfp_fft_plan_set_timing(gfp_fft_plan *plan, int on);
 int gfp_fft_plan_pass_times(gfp_fft_plan *plan, float *ms, int *pass, int max);
 
-/* Number of transform pass launches of this process that ran as the TMA form
-   of the k = 8 pass (k_pass44t: cp.async.bulk.tensor tile loads / stores;
-   gfp_pass44t.cuh) -- lets a test or the benchmark confirm which kernel
+/* Number of transform launches of this process that ran as one of the
+   TMA-tile kernels (cp.async.bulk.tensor tile loads / stores): the k = 8 pass
+   k_pass44t (gfp_pass44t.cuh), the k = 16 first pass k_first16t
+   (gfp_pass16t.cuh), the fused middle of a poly-multiply k_pmid44t
+   (gfp_pmid44t.cuh) -- lets a test or the benchmark confirm which kernel
    served a transform. */
 int64_t gfp_tma_pass_launches(void);
 
