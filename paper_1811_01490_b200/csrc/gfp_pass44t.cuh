@@ -42,6 +42,14 @@
 #ifndef P44T_UNROLL_A_MAXEPT
 #define P44T_UNROLL_A_MAXEPT 0  // phase-A loop unrolled up to this many elements per thread
 #endif
+#ifndef P44T_TRACE
+#define P44T_TRACE 0  // timeline of CTA (0, 0)'s warp 0 by printf (tools only)
+#endif
+#if P44T_TRACE
+#define P44T_T(i) do { if (trace_on) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr[i])); } while (0)
+#else
+#define P44T_T(i) ((void)0)
+#endif
 #ifndef P44T_EVICT_FIRST
 #define P44T_EVICT_FIRST 1  // streamed tiles carry an L2 evict-first policy (tables stay)
 #endif
@@ -165,6 +173,11 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
     const int j0 = blockIdx.x * 32;  // M % 32 == 0: every lane has a group
     const int64_t j = j0 + lane;
 
+#if P44T_TRACE
+    unsigned long long tr[10] = {0};
+    const bool trace_on = blockIdx.x == 1 && blockIdx.y == 0 && threadIdx.x == 0;
+#endif
+    P44T_T(0);
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int t = 0; t < K; t++)
@@ -176,6 +189,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
     // writes are visible after the wait, before the first tile load
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    P44T_T(1);
     const u64 pol = p44t::evict_first_policy();
     if (leader) {
 #pragma unroll
@@ -243,6 +257,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
             }
         }
         p44t::mbar_wait(&bar[t], 0);
+        if (i == 0)
+            P44T_T(2);
         i64 x[KD], f[KD];
 #pragma unroll
         for (int d = 0; d < KD; d++)
@@ -266,6 +282,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
         }
     }
 
+    P44T_T(3);
     GFP_JITTER(1);
     // ---- stage 1 (warps w < 4, t1 = w): 4-point DFT over t2 of tiles
     // t1 + 4 t2, outputs u0 back into tiles t1 + 4 u0 -- the same four tiles.
@@ -273,6 +290,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
     i64 e[4][KD];
     if (NW > 4)
         __syncthreads();
+    P44T_T(4);
     if (w < 4) {
 #pragma unroll
         for (int t2 = 0; t2 < 4; t2++) {
@@ -290,8 +308,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
                 tile[d * 32] = e[u0][d];
         }
     }
+    P44T_T(5);
     GFP_JITTER(2);
     __syncthreads();
+    P44T_T(6);
 
     // ---- stage 2 over SPL = NW / 4 warps per u0: every warp gathers
     // Y[t1][u0] from tiles 4 u0 + t1, applies rho^(t1 u0) as a compile-time
@@ -397,6 +417,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
         for (int d = 0; d < KD; d++)
             tile[GFP_IDX(d * os, TILE - ob)] = e[q][d];
     }
+    P44T_T(7);
     // generic-proxy writes -> async proxy (TMA) reads
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
@@ -418,6 +439,13 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
         // the tiles must stay until the stores have read them
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     }
+#if P44T_TRACE
+    P44T_T(8);
+    if (trace_on)
+        printf("P44T_TRACE NW=%d lNs=%d start=%llu init+pdlwait=%llu tilewait=%llu phaseA=%llu bar1=%llu stage1=%llu bar2=%llu stage2=%llu store=%llu\n",
+               NW, lNs, tr[0], tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2], tr[4] - tr[3], tr[5] - tr[4],
+               tr[6] - tr[5], tr[7] - tr[6], tr[8] - tr[7]);
+#endif
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no link
