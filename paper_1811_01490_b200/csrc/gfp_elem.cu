@@ -99,7 +99,18 @@ static bool fast_bounds(int k, u64 r, FastPlan *out)
             return false;
         fp.S = S;
         u128 q1, ex1;
-        norm_bounds(X << S, r, fp, &q1, &ex1);
+        // the digits entering the S lazy stages: normalised ones, or -- mode 3
+        // with the rounding column quotient (k <= 8, gfp_fast.cuh) -- products
+        // of magnitude up to 3r/4
+        u128 Vn = X << S;
+        if (k <= 8 && r == p2_radix_of(k)) {
+            const u128 Xm = 3 * ((u128)r / 4) + 16;
+            if ((Xm << S) + top >= two63)
+                return false;
+            if ((Xm << S) > Vn)
+                Vn = Xm << S;
+        }
+        norm_bounds(Vn, r, fp, &q1, &ex1);
         // multiply: balanced limbs, |xl| <= 2^(s-1), |xh| <= H, |xs| <= 2^(s-1) + H
         u128 H = (X + half) >> s;
         u128 Hs = half + H;
@@ -205,6 +216,31 @@ RadixConsts make_consts(int k, u64 r)
             norm_bounds(3 * (u128)r, r, fp, &q2, &ex2);
             norm_bounds(X + cmax, r, fp, &q0, &ex0);
             ok = ok && ex0 <= fp.delta && ex2 + q0 <= fp.delta;
+            // k <= 8: the rounding column quotient (column_quot_p3r).  A multiply's
+            // x operand is a normalised digit vector or an earlier product
+            // (|x| <= Xm = 3r/4 + 16), its y operand a table entry or a
+            // normalised vector (|y| <= X)
+            if (k <= 8 && ok) {
+                const u128 Xm = 3 * ((u128)r / 4) + 16;
+                const u128 Hx = (Xm + half) >> S, Hy = (X + half) >> S;
+                const u128 cr = kk * Xm * X / r + 16;                  // |carry|
+                const u128 llc = kk * half * half + cr;                // |LL + C|
+                const u128 mid = kk * half * (Hx + Hy) + (llc >> S) + 2;  // |MID + (LL >> S)|
+                const u128 cabs2 = kk * Xm * X + cr;
+                const int e2r = a - 2 + 2 * (a - b) - 8;
+                ok = 2 * S >= a - 2 && a - 2 >= S && llc < two63 &&
+                     kk * (half + Hx) * (half + Hy) < two63 &&          // SS, SS - SSn
+                     mid < two63 &&
+                     ((kk * Hx * Hy) << (2 * S - (a - 2))) + (mid >> (a - 2 - S)) + 4 < two63 &&  // T4, q4 + 2
+                     (e2r >= 127 || (cabs2 >> e2r) == 0) &&             // second-order term < 1/256
+                     Xm + cr + ((u128)1 << (a - 1)) < two63 &&          // digit 0: norm_bal(d_0 - C)
+                     (Xm << fp.S) + ((u128)1 << (a - 1)) < two63;       // lazy stages + normalize_el
+                // digit 0 comes out of norm_bal (balanced, within delta); digit 1
+                // gets its carry on top of a product digit
+                u128 q0r, ex0r;
+                norm_bounds(Xm + cr, r, fp, &q0r, &ex0r);
+                ok = ok && ex0r <= fp.delta && q0r + 3 * ((u128)r / 4) + 2 <= Xm;
+            }
             // the k = 32 mode-3 pass runs its 64-point DFT without a mid normalisation
             ok = ok && (k != 32 || fp.S >= 6);
             c.p3_ok = ok ? 1 : 0;

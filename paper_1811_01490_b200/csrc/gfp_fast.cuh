@@ -113,12 +113,42 @@ GFP_D i64 column_quot_p3(i64 LL, i64 MID, i64 HH, u64 &rem)
     return q;
 }
 
+// Mode 3 quotient with the rounding folded in (k <= 8, GFP_P3_ROUNDQ): the
+// quotient estimate is taken at a quarter of a digit,
+//   T4 = floor(c / 2^(a-2)),  q4 = T4 - floor(T4 2^(b-a)),  4 c / r - q4 in (-1, 1),
+// and rounded to the nearest integer, q = floor((q4 + 2) / 4), so
+//   c / r - q in (-3/4, 3/4):  rem = c - q r is already a balanced digit,
+// |rem| < 3r/4, and the second carry round (norm_bal of the remainder) is
+// gone.  Three quarters of r instead of a half costs nothing downstream: four
+// lazy radix-2 stages of such digits stay below 12 r + r/2 < 2^63 (the host
+// check in make_consts, gfp_elem.cu, proves every bound for the radix).
+template <int S, int KD>
+GFP_D i64 column_quot_p3r(i64 LL, i64 MID, i64 HH, u64 &rem)
+{
+    constexpr int a = P2Radix<KD>::a, b = P2Radix<KD>::b;
+    static_assert(2 * S >= a - 2 && a - 2 >= S && a - 2 - S < 32 && 2 * S - (a - 2) < 8,
+                  "P2Radix vs S (rounding quotient)");
+    const i64 mid = MID + (LL >> S);                                       // floor(c / 2^S) - HH 2^S
+    const i64 T4 = (HH << (2 * S - (a - 2))) + (mid >> ((a - 2) - S));     // floor(c / 2^(a-2))
+    const i64 q4 = T4 - (T4 >> (a - b));
+    const i64 q = (q4 + 2) >> 2;
+    const u64 clo = (u64)LL + ((u64)MID << S) + ((u64)HH << (2 * S));
+    rem = clo - ((u64)q << a) - ((u64)q << b);
+    return q;
+}
+
+#ifndef GFP_P3_ROUNDQ
+#define GFP_P3_ROUNDQ 1  // mode 3, k <= 8: rounding column quotient (no norm_bal per column)
+#endif
+
 // The carry rounds of one product, column by column (m = 0 .. k-1), shared
 // by the multiply kernels.  Column m's value is c_m = HH 2^(2S) + MID 2^S + LL.
 //   modes 0-2:  c_m = q_m r + d_m (column_quot*, d_m in [0, 4r)), then
 //               d_m + q_{m-1} = q2_m r + d2_m (norm_bal), digit = d2_m + q2_{m-1}
-//   mode 3, k <= 8 (SEQ): sequential carry: c_m + C_{m-1} = q_m r + rem_m,
-//               rem_m = q2_m r + d_m (norm_bal), digit = d_m, C_m = q_m + q2_m
+//   mode 3, k <= 8 (SEQ): sequential carry: c_m + C_{m-1} = q_m r + rem_m with
+//               the rounding quotient (column_quot_p3r): digit = rem_m,
+//               |rem_m| < 3r/4, C_m = q_m  [without GFP_P3_ROUNDQ:
+//               rem_m = q2_m r + d_m (norm_bal), digit = d_m, C_m = q_m + q2_m]
 //               (one carry round less; for k >= 16 the serial chain across a
 //               block of columns costs more than it saves -- measured: the
 //               window multiplies keep the two-round form)
@@ -133,10 +163,15 @@ struct ColReduce {
     {
         if constexpr (SEQ) {
             u64 rem;
-            const i64 q = column_quot_p3<S, KD>(LL + q_prev, MID, HH, rem);
             i64 d;
-            const int q2 = norm_bal<3, KD>((i64)rem, rc, d);
-            q_prev = q + q2;
+            if constexpr (GFP_P3_ROUNDQ) {
+                q_prev = column_quot_p3r<S, KD>(LL + q_prev, MID, HH, rem);
+                d = (i64)rem;  // |d| < 3r/4
+            } else {
+                const i64 q = column_quot_p3<S, KD>(LL + q_prev, MID, HH, rem);
+                const int q2 = norm_bal<3, KD>((i64)rem, rc, d);
+                q_prev = q + q2;
+            }
             if (m == 0) {
                 d0 = d;
                 return false;
