@@ -531,7 +531,7 @@ int launch_pass(const gfp_fft_plan *p, const u64 *in, u64 *out, const u64 *in2,
         return err;
     // large k = 8 transforms: the TMA form of the pass for every pass it takes
     if (pass44_enabled(KD, A.rc) &&
-        p44t_takes(A, p->M, ((p->M + 31) / 32) * (in2 ? 2 * batch : batch)) &&
+        p44t_takes(A, p->M) &&
         launch_pass44t<KD>(A, p->M, in2 ? 2 * batch : batch, st))
         return cuda_status();
     if (launch_pass44<KD>(A, p->M, in2 ? 2 * batch : batch, st))

@@ -39,19 +39,13 @@
 #define P44T_EARLY_TABLE_MINEPT 4  // elements per thread from which the table entry is loaded
                                    // before the tile wait
 #endif
-#ifndef P44T_UNROLL_A_MAXEPT
-#define P44T_UNROLL_A_MAXEPT 0  // phase-A loop unrolled up to this many elements per thread
-#endif
 #ifndef P44T_TRACE
-#define P44T_TRACE 0  // timeline of CTA (0, 0)'s warp 0 by printf (tools only)
+#define P44T_TRACE 0  // timeline of one CTA by printf (tools/trace_c2.py only)
 #endif
 #if P44T_TRACE
 #define P44T_T(i) do { if (trace_on) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr[i])); } while (0)
 #else
 #define P44T_T(i) ((void)0)
-#endif
-#ifndef P44T_EVICT_FIRST
-#define P44T_EVICT_FIRST 1  // streamed tiles carry an L2 evict-first policy (tables stay)
 #endif
 
 // tensor maps of one pass launch: the two vector sets' inputs and outputs
@@ -112,33 +106,20 @@ GFP_D u64 evict_first_policy()
 // box {c0 .. c0 + 31, all rows, batch c2} -> dst, completion on bar
 GFP_D void tma_load(void *dst, const CUtensorMap *map, u64 *bar, int c0, int c2, u64 pol)
 {
-#if P44T_EVICT_FIRST
+    // streamed tiles carry an L2 evict-first policy: the twiddle tables stay
+    // (without it: C4 4.35 -> 4.51 ms)
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(0), "r"(c2), "l"(pol)
         : "memory");
-#else
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(0), "r"(c2)
-        : "memory");
-#endif
 }
 GFP_D void tma_store(const CUtensorMap *map, const void *src, int c0, int c2, u64 pol)
 {
-#if P44T_EVICT_FIRST
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group.L2::cache_hint"
                  " [%0, {%2, %3, %4}], [%1], %5;" ::"l"(map),
                  "r"(smem_u32(src)), "r"(c0), "r"(0), "r"(c2), "l"(pol)
                  : "memory");
-#else
-    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group"
-                 " [%0, {%2, %3, %4}], [%1];" ::"l"(map),
-                 "r"(smem_u32(src)), "r"(c0), "r"(0), "r"(c2)
-                 : "memory");
-#endif
 }
 
 }  // namespace p44t
@@ -204,8 +185,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? P44T_MINB : NW == 8 ? 2 : 1
     // r^a omega^b; r^a is the row the digit is read from (and a sign folded
     // into the multiply's limb split), omega^b one general multiply whose
     // digits go back to the tile as they become final
-    constexpr int UNR_A = EPT <= P44T_UNROLL_A_MAXEPT ? EPT : 1;
-#pragma unroll UNR_A
+#pragma unroll 1
     for (int i = 0; i < EPT; i++) {
         const int t = w + NW * i;
         i64 *tile = sm + GFP_IDX(t * TILE + lane, K * TILE);
@@ -529,15 +509,9 @@ static inline bool p44t_make_map(CUtensorMap *m, const u64 *base, int64_t N, int
 // the passes k_pass44t takes: the digit-major k = 8 passes of transforms
 // with at least 32 groups (not the pointwise-product, host-memory or
 // fused-exchange forms of the first / last pass)
-#ifndef P44T_FIRST
-#define P44T_FIRST 0  // 0: the first pass (Ns = 1) too; -1: it stays on k_pass44 (A/B builds)
-#endif
-#ifndef P44T_MIN_CTAS
-#define P44T_MIN_CTAS 0  // smallest grid routed here (A/B builds)
-#endif
-static inline bool p44t_takes(const PassArgs &A, int64_t M, int64_t ctas)
+static inline bool p44t_takes(const PassArgs &A, int64_t M)
 {
-    return P44_TMA && ctas >= P44T_MIN_CTAS && (M & 31) == 0 && (A.lNs >= 4 || A.lNs == P44T_FIRST) &&
+    return P44_TMA && (M & 31) == 0 && (A.lNs >= 4 || A.lNs == 0) &&
            A.lN <= 30 && A.ft_lN <= 30 && !A.in_em && !A.out_em && !A.xg && !A.pre;
 }
 
