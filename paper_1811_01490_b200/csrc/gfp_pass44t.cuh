@@ -33,7 +33,10 @@
 #define P44_TMA 1  // 0: large transforms stay on k_pass44<NW = 4> (A/B builds)
 #endif
 #ifndef P44T_MINB
-#define P44T_MINB 5  // CTAs per SM the kernel is register-bounded for (32 KB tiles each)
+#define P44T_MINB 6  // CTAs per SM the NW = 4 kernel is register-bounded for (32 KB tiles
+                     // each): 80 registers with 192 B of spills beats 5 CTAs at 96 since the
+                     // rounding column quotient (C4 passes 0.698 -> 0.678 ms); 4 CTAs at 126
+                     // registers: 0.70 ms
 #endif
 #ifndef P44T_EARLY_TABLE_MINEPT
 #define P44T_EARLY_TABLE_MINEPT 4  // elements per thread from which the table entry is loaded
