@@ -100,10 +100,10 @@ static bool fast_bounds(int k, u64 r, FastPlan *out)
         fp.S = S;
         u128 q1, ex1;
         // the digits entering the S lazy stages: normalised ones, or -- mode 3
-        // with the rounding column quotient (k <= 8, gfp_fast.cuh) -- products
+        // with the rounding column quotient (k <= GFP_SEQ_MAXK, gfp_fast.cuh) -- products
         // of magnitude up to 3r/4
         u128 Vn = X << S;
-        if (k <= 8 && r == p2_radix_of(k)) {
+        if (k <= GFP_SEQ_MAXK && r == p2_radix_of(k)) {
             const u128 Xm = 3 * ((u128)r / 4) + 16;
             if ((Xm << S) + top >= two63)
                 return false;
@@ -216,11 +216,11 @@ RadixConsts make_consts(int k, u64 r)
             norm_bounds(3 * (u128)r, r, fp, &q2, &ex2);
             norm_bounds(X + cmax, r, fp, &q0, &ex0);
             ok = ok && ex0 <= fp.delta && ex2 + q0 <= fp.delta;
-            // k <= 8: the rounding column quotient (column_quot_p3r).  A multiply's
+            // k <= GFP_SEQ_MAXK: the rounding column quotient (column_quot_p3r).  A multiply's
             // x operand is a normalised digit vector or an earlier product
             // (|x| <= Xm = 3r/4 + 16), its y operand a table entry or a
             // normalised vector (|y| <= X)
-            if (k <= 8 && ok) {
+            if (k <= GFP_SEQ_MAXK && ok) {
                 const u128 Xm = 3 * ((u128)r / 4) + 16;
                 const u128 Hx = (Xm + half) >> S, Hy = (X + half) >> S;
                 const u128 cr = kk * Xm * X / r + 16;                  // |carry|

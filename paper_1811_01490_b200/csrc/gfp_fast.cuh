@@ -113,7 +113,7 @@ GFP_D i64 column_quot_p3(i64 LL, i64 MID, i64 HH, u64 &rem)
     return q;
 }
 
-// Mode 3 quotient with the rounding folded in (k <= 8, GFP_P3_ROUNDQ): the
+// Mode 3 quotient with the rounding folded in (k <= GFP_SEQ_MAXK, GFP_P3_ROUNDQ): the
 // quotient estimate is taken at a quarter of a digit,
 //   T4 = floor(c / 2^(a-2)),  q4 = T4 - floor(T4 2^(b-a)),  4 c / r - q4 in (-1, 1),
 // and rounded to the nearest integer, q = floor((q4 + 2) / 4), so
@@ -137,6 +137,11 @@ GFP_D i64 column_quot_p3r(i64 LL, i64 MID, i64 HH, u64 &rem)
     return q;
 }
 
+#ifndef GFP_SEQ_MAXK
+#define GFP_SEQ_MAXK 32  // largest k whose mode-3 multiply folds the carry into the next column
+                         // (with the rounding quotient the serial chain is short enough for
+                         // k = 16 / 32 too: C3 multiply passes -3.7%, C5 FFT -1.5%)
+#endif
 #ifndef GFP_P3_ROUNDQ
 #define GFP_P3_ROUNDQ 1  // mode 3, k <= 8: rounding column quotient (no norm_bal per column)
 #endif
@@ -145,17 +150,17 @@ GFP_D i64 column_quot_p3r(i64 LL, i64 MID, i64 HH, u64 &rem)
 // by the multiply kernels.  Column m's value is c_m = HH 2^(2S) + MID 2^S + LL.
 //   modes 0-2:  c_m = q_m r + d_m (column_quot*, d_m in [0, 4r)), then
 //               d_m + q_{m-1} = q2_m r + d2_m (norm_bal), digit = d2_m + q2_{m-1}
-//   mode 3, k <= 8 (SEQ): sequential carry: c_m + C_{m-1} = q_m r + rem_m with
+//   mode 3, k <= GFP_SEQ_MAXK (SEQ): sequential carry: c_m + C_{m-1} = q_m r + rem_m with
 //               the rounding quotient (column_quot_p3r): digit = rem_m,
 //               |rem_m| < 3r/4, C_m = q_m  [without GFP_P3_ROUNDQ:
 //               rem_m = q2_m r + d_m (norm_bal), digit = d_m, C_m = q_m + q2_m]
-//               (one carry round less; for k >= 16 the serial chain across a
-//               block of columns costs more than it saves -- measured: the
-//               window multiplies keep the two-round form)
+//               (before the rounding quotient the serial chain across a block of
+//               columns cost more than it saved for k >= 16; with it the chain
+//               is short enough and every k takes this form)
 // with the r^k = -1 wrap at m = 0 resolved by finish() (digits 0 and 1).
 template <int S, int SPARSE, int KD>
 struct ColReduce {
-    static constexpr bool SEQ = SPARSE == 3 && KD <= 8;
+    static constexpr bool SEQ = SPARSE == 3 && KD <= GFP_SEQ_MAXK;
     i64 q_prev = 0, d0 = 0, f1 = 0;
     int q2_prev = 0;
     // returns true when digit m (>= 2) is final in `out`
