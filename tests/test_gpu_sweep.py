@@ -1,0 +1,94 @@
+"""Shape sweep of the transform kernels: batch sizes on both sides of every
+CTA-shape threshold (k_pass44t NW = 16 / 8 / 4 by grid size, two vector sets
+per launch, the fused poly-multiply middle with grid.y > 1, k_first16t), each
+batched call compared row by row with the single-row call of the same
+library, and sampled rows with the oracle (dft_general / dft_inverse,
+fft.py:298-370; the poly-multiply composition of SURVEY 3.4)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+R8 = (1 << 59) + (1 << 16)
+R16 = (1 << 58) + (1 << 10)
+
+
+def _eq(a, b):
+    import torch
+    return a.shape == b.shape and torch.equal(a.view(torch.int64), b.view(torch.int64))
+
+
+def _setup(k, r, K, e):
+    import paper_1811_01490_b200 as gp
+    from oracle import oracle as O
+    params = gp.GfpParams(r, k)
+    field = gp.GfpFftField(params, backend="cuda")
+    omega = gp.roots_for(params, K ** e)
+    plan = gp.build_plan(field, K, e, omega)
+    return gp, O, params, plan, O.Plan(k, r, K, e, omega)
+
+
+@pytest.mark.parametrize("e,batches", [(2, (1, 3, 40)), (3, (1, 7, 18, 19, 37, 73, 74, 75)),
+                                       (4, (1, 2, 3, 5))],
+                         ids=["n256", "n4096", "n65536"])
+def test_k8_transform_batches(e, batches, cuda):
+    gp, O, params, plan, oplan = _setup(8, R8, 16, e)
+    N = 16 ** e
+    for B in batches:
+        x = gp.vec.uniform(N, params, seed=900 + B, batch=B) if B > 1 else \
+            gp.vec.uniform(N, params, seed=900 + B).unsqueeze(0)
+        y = gp.fft_tensor(x, plan)
+        z = gp.fft_tensor(x, plan, inverse=True)
+        for b in sorted({0, B // 2, B - 1}):
+            assert _eq(gp.fft_tensor(x[b], plan), y[b]), (e, B, b)
+            assert _eq(gp.fft_tensor(x[b], plan, inverse=True), z[b]), (e, B, b)
+        xb = gp.vec.to_host(x[B - 1])
+        assert np.array_equal(gp.vec.to_host(y[B - 1]), oplan.forward(xb)), (e, B)
+        assert np.array_equal(gp.vec.to_host(z[B - 1]), oplan.inverse(xb)), (e, B)
+        # round trip of the whole batch
+        assert _eq(gp.fft_tensor(y, plan, inverse=True), x), (e, B)
+
+
+@pytest.mark.parametrize("e,batches", [(2, (1, 5)), (3, (1, 2, 9, 37, 38)), (4, (1, 3))],
+                         ids=["n256", "n4096", "n65536"])
+def test_k8_poly_mul_batches(e, batches, cuda):
+    """Batched poly-multiplies (the fused middle kernel with grid.y = batch for
+    N >= 512, the two-kernel middle below) against the single product and the
+    oracle."""
+    gp, O, params, plan, oplan = _setup(8, R8, 16, e)
+    N = 16 ** e
+    for B in batches:
+        import torch
+        f = gp.vec.uniform(N, params, seed=1300 + B, batch=max(B, 2)).view(torch.int64)[:B] \
+            .contiguous().view(torch.uint64)
+        g = gp.vec.uniform(N, params, seed=1400 + B, batch=max(B, 2)).view(torch.int64)[:B] \
+            .contiguous().view(torch.uint64)
+        h = gp.poly_mul(f, g, plan)
+        for b in sorted({0, B // 2, B - 1}):
+            assert _eq(gp.poly_mul(f[b], g[b], plan), h[b]), (e, B, b)
+        got = gp.vec.to_host(h[B - 1])
+        want = oplan.poly_mul(gp.vec.to_host(f[B - 1]), gp.vec.to_host(g[B - 1]))
+        assert np.array_equal(got, want), (e, B)
+        # out aliasing an operand
+        f2 = f.view(torch.int64).clone().view(torch.uint64)
+        gp.poly_mul(f2, g, plan, out=f2)
+        assert _eq(f2, h), (e, B)
+
+
+@pytest.mark.parametrize("e,batches", [(2, (1, 3, 10)), (3, (1, 2, 5))], ids=["n1024", "n32768"])
+def test_k16_transform_batches(e, batches, cuda):
+    gp, O, params, plan, oplan = _setup(16, R16, 32, e)
+    N = 32 ** e
+    for B in batches:
+        x = gp.vec.uniform(N, params, seed=1700 + B, batch=B) if B > 1 else \
+            gp.vec.uniform(N, params, seed=1700 + B).unsqueeze(0)
+        y = gp.fft_tensor(x, plan)
+        z = gp.fft_tensor(x, plan, inverse=True)
+        for b in sorted({0, B - 1}):
+            assert _eq(gp.fft_tensor(x[b], plan), y[b]), (e, B, b)
+        xb = gp.vec.to_host(x[B - 1])
+        assert np.array_equal(gp.vec.to_host(y[B - 1]), oplan.forward(xb)), (e, B)
+        assert np.array_equal(gp.vec.to_host(z[B - 1]), oplan.inverse(xb)), (e, B)
+        assert _eq(gp.fft_tensor(y, plan, inverse=True), x), (e, B)
+        h = gp.poly_mul(x, x, plan)
+        assert np.array_equal(gp.vec.to_host(h[B - 1]), oplan.poly_mul(xb, xb)), (e, B)
