@@ -300,6 +300,16 @@ int gfp_fft_plan_caps(const gfp_fft_plan *plan);
 int gfp_fft_plan_set_timing(gfp_fft_plan *plan, int on);
 int gfp_fft_plan_pass_times(gfp_fft_plan *plan, float *ms, int *pass, int max);
 
+/* Which arithmetic mode the transform / multiply kernels take for (k, r), as
+   decided by the host-side bound proofs (make_consts: exact integer bounds on
+   every sub-column, carry and lazy stage of the multiply and the butterflies):
+   3 -- compile-time radix r = 2^a + 2^b (the paper's radices; shift quotients,
+        sequential carry with the rounding column quotient);
+   2 -- r = 2^a + 2^b at run time;  1 -- sparse r = 2^a + eps;  0 -- reciprocal
+        quotient;  -1 -- no lazy-digit headroom (the generic canonical-digit
+        path);  -2 for an invalid (k, r).  Host only: needs no GPU. */
+int gfp_radix_mode(int k, uint64_t r);
+
 /* Number of transform launches of this process that ran as one of the
    TMA-tile kernels (cp.async.bulk.tensor tile loads / stores): the k = 8 pass
    k_pass44t (gfp_pass44t.cuh), the k = 16 first pass k_first16t

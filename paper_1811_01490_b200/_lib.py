@@ -86,6 +86,7 @@ SIGNATURES = {
     "gfp_ipc_get_handle": (_int, [_vp, ctypes.c_char_p, ctypes.POINTER(_i64)]),
     "gfp_ipc_open": (_int, [ctypes.c_char_p, _i64, ctypes.POINTER(_vp)]),
     "gfp_ipc_close": (_int, [_vp, _i64]),
+    "gfp_radix_mode": (_int, [_int, _u64]),
     "gfp_tma_pass_launches": (_i64, []),
     "gfp_debug_build": (_int, []),
     "gfp_debug_selftest": (_int, [_vp]),

@@ -587,6 +587,16 @@ int check_kr(int k, u64 r)
 
 extern "C" {
 
+int gfp_radix_mode(int k, uint64_t r)
+{
+    if (check_kr(k, r))
+        return -2;
+    const RadixConsts c = make_consts(k, r);
+    if (c.stages_per_norm <= 0)
+        return -1;
+    return c.p3_ok ? 3 : c.p2_ok ? 2 : c.sp_on ? 1 : 0;
+}
+
 int gfp_vec_add(const uint64_t *x, const uint64_t *y, uint64_t *z, int64_t n, int k, uint64_t r,
                 void *stream)
 {

@@ -96,3 +96,22 @@ def test_oracle_element_ops_property():
         assert dec(O.mul(X, Y, r, backend="school")) == [a * b % p for a, b in zip(xs, ys)]
         i = rng.randrange(2 * k + 1)
         assert dec(O.mul_pow_r(X, r, i)) == [a * pow(r, i, p) % p for a in xs]
+
+
+def test_radix_mode_host_bound_proofs():
+    """gfp_radix_mode runs the host-side bound proofs (make_consts): the
+    paper's radices (bench_cli.py:36-41) take the compile-time mode 3 -- which
+    includes the proof of the rounding column quotient's bounds --, other
+    r = 2^a + 2^b the run-time mode 2, a radix near 2^64 has no lazy-digit
+    headroom (the generic canonical path), invalid (k, r) are rejected."""
+    from paper_1811_01490_b200 import _lib
+    lib = _lib.load()
+    assert lib.gfp_radix_mode(8, (1 << 59) + (1 << 16)) == 3
+    assert lib.gfp_radix_mode(16, (1 << 58) + (1 << 10)) == 3
+    assert lib.gfp_radix_mode(32, (1 << 56) + (1 << 21)) == 3
+    assert lib.gfp_radix_mode(8, (1 << 58) + (1 << 12)) == 2   # not the k = 8 radix
+    assert lib.gfp_radix_mode(16, (1 << 59) + (1 << 16)) == -1  # k = 8's radix at k = 16: no headroom
+    assert lib.gfp_radix_mode(8, (1 << 63) + (1 << 34)) == -1
+    assert lib.gfp_radix_mode(4, (1 << 64) - (1 << 50)) == -1
+    assert lib.gfp_radix_mode(8, 12345678901234567) == 0        # no sparse structure
+    assert lib.gfp_radix_mode(3, 1000) == -2 and lib.gfp_radix_mode(8, 1) == -2
