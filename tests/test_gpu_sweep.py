@@ -92,3 +92,87 @@ def test_k16_transform_batches(e, batches, cuda):
         assert _eq(gp.fft_tensor(y, plan, inverse=True), x), (e, B)
         h = gp.poly_mul(x, x, plan)
         assert np.array_equal(gp.vec.to_host(h[B - 1]), oplan.poly_mul(xb, xb)), (e, B)
+
+
+# GFP primes p = r^8 + 1 outside the reference's list (found by a Miller-Rabin
+# search over r = 2^a + 2^b and random even r): the run-time arithmetic modes
+# of the fast path (gfp_radix_mode 1: sparse radix, 0: reciprocal quotient)
+OTHER_R8 = [((1 << 56) + (1 << 28), 1), ((1 << 57) + (1 << 38), 0), (71234253391507836, 0),
+            ((1 << 44) + (1 << 16), 1)]
+
+
+@pytest.mark.parametrize("r,mode", OTHER_R8, ids=["2^56+2^28", "2^57+2^38", "random56", "2^44+2^16"])
+def test_k8_other_prime_radices_run_time_modes(r, mode, cuda):
+    """The reference's build_plan accepts any GFP prime (fft.py:237-275).  For
+    k = 8 radices other than the paper's, the same pass kernels (k_pass44t,
+    k_pmid44t, k_pass44) run in their run-time-radix instantiations: forward,
+    inverse, batched, poly-multiply and the host entry against the oracle
+    (schoolbook products)."""
+    import torch
+    import paper_1811_01490_b200 as gp
+    from oracle import oracle as O
+    from paper_1811_01490_b200 import _lib
+    lib = _lib.load()
+    assert lib.gfp_radix_mode(8, r) == mode
+    k, K, e = 8, 16, 3
+    N = K ** e
+    params = gp.GfpParams(r, k)
+    field = gp.GfpFftField(params, backend="cuda")
+    omega = gp.roots_for(params, N)
+    plan = gp.build_plan(field, K, e, omega)
+    oplan = O.Plan(k, r, K, e, np.array(omega, dtype=np.uint64), backend="school")
+    B = 20  # 160 CTAs: the NW = 8 shape; single rows take NW = 16
+    x = O.random_elements(7000 + mode, k, r, B * N).reshape(B, N, k)
+    xd = torch.stack([gp.vec.to_device(x[b], k) for b in range(B)])
+    before = lib.gfp_tma_pass_launches()
+    y = gp.fft_tensor(xd, plan)
+    z = gp.fft_tensor(xd, plan, inverse=True)
+    assert lib.gfp_tma_pass_launches() - before == 6
+    for b in (0, B - 1):
+        assert np.array_equal(gp.vec.to_host(y[b]), oplan.forward(x[b])), b
+        assert np.array_equal(gp.vec.to_host(z[b]), oplan.inverse(x[b])), b
+        assert _eq(gp.fft_tensor(xd[b], plan), y[b]), b
+    assert _eq(gp.fft_tensor(y, plan, inverse=True), xd)
+    f = np.zeros((N, k), dtype=np.uint64)
+    g = f.copy()
+    f[: N // 2] = x[0][: N // 2]
+    g[: N // 3] = x[1][: N // 3]
+    want = oplan.poly_mul(f, g)
+    got = gp.vec.to_host(gp.poly_mul(gp.vec.to_device(f, k), gp.vec.to_device(g, k), plan))
+    assert np.array_equal(got, want)
+    assert np.array_equal(gp.poly_mul_host(f[: N // 2], g[: N // 3], plan),
+                          want[: N // 2 + N // 3 - 1])
+    # element-wise multiply in the same mode
+    a, b2 = x[2][:1000], x[3][:1000]
+    prod = gp.vec.to_host(gp.vec.mul(gp.vec.to_device(a, k), gp.vec.to_device(b2, k), params))
+    assert np.array_equal(prod, O.mul(a, b2, r, backend="school"))
+
+
+@pytest.mark.parametrize("r,mode", [((1 << 52) + (1 << 22), 1), ((1 << 52) + (1 << 34), 0)],
+                         ids=["2^52+2^22", "2^52+2^34"])
+def test_k16_other_prime_radices_run_time_modes(r, mode, cuda):
+    """GFP primes p = r^16 + 1 outside the reference's list: k_pass<16> in its
+    run-time-radix instantiations against the oracle (schoolbook products)."""
+    import torch
+    import paper_1811_01490_b200 as gp
+    from oracle import oracle as O
+    from paper_1811_01490_b200 import _lib
+    assert _lib.load().gfp_radix_mode(16, r) == mode
+    k, K, e = 16, 32, 2
+    N = K ** e
+    params = gp.GfpParams(r, k)
+    field = gp.GfpFftField(params, backend="cuda")
+    omega = gp.roots_for(params, N)
+    plan = gp.build_plan(field, K, e, omega)
+    oplan = O.Plan(k, r, K, e, np.array(omega, dtype=np.uint64), backend="school")
+    x = O.random_elements(7100 + mode, k, r, 3 * N).reshape(3, N, k)
+    xd = torch.stack([gp.vec.to_device(x[b], k) for b in range(3)])
+    y = gp.fft_tensor(xd, plan)
+    z = gp.fft_tensor(xd, plan, inverse=True)
+    for b in range(3):
+        assert np.array_equal(gp.vec.to_host(y[b]), oplan.forward(x[b])), b
+        assert np.array_equal(gp.vec.to_host(z[b]), oplan.inverse(x[b])), b
+    h = gp.poly_mul(xd[0], xd[1], plan)
+    assert np.array_equal(gp.vec.to_host(h), oplan.poly_mul(x[0], x[1]))
+    prod = gp.vec.to_host(gp.vec.mul(xd[0], xd[1], params))
+    assert np.array_equal(prod, O.mul(x[0], x[1], r, backend="school"))
