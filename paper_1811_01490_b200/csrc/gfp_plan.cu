@@ -673,7 +673,8 @@ int gfp_poly_mul(const gfp_fft_plan *cp, const uint64_t *f, const uint64_t *g, u
             err = run_generic(p, f + b0 * ew, o, scratch, nb, 0, st);
             if (!err)
                 err = run_generic(p, g + b0 * ew, G, scratch_b, nb, 0, st);
-        } else if (poly_mid_supported(p)) {
+        } else if (poly_mid_supported(p) &&
+                   !(((uintptr_t)o | (uintptr_t)G | (uintptr_t)scratch | (uintptr_t)scratch_b) & 15)) {
             // forward passes 0 .. e-2 of both operands, then ONE kernel for the
             // forward last pass + pointwise product + inverse first pass, then
             // the inverse passes 1 .. e-1 (2 e - 1 launches instead of 2 e)
@@ -796,7 +797,8 @@ int gfp_poly_mul_host2(gfp_fft_plan *p, const uint64_t *f, int64_t nf, const uin
     // the element-major operands (zero past nf / ng); spectra stay lazy
     PassIO e1 = {mf, mg, nf, ng, nullptr, 0, nullptr, 0, 0};
     PassIO e2 = {nullptr, nullptr, 0, 0, dout, n_out, nullptr, 0, 0};
-    if (poly_mid_supported(p)) {  // the middle as one kernel (gfp_pmid44t.cuh)
+    if (poly_mid_supported(p) &&  // the middle as one kernel (gfp_pmid44t.cuh; TMA: 16 B alignment)
+        !(((uintptr_t)F | (uintptr_t)G | (uintptr_t)s1 | (uintptr_t)s2) & 15)) {
         err = poly_mul_fused(p, F, G, F, G, s1, s2, batch, st, &e1, &e2);
     } else {
         err = run_transform2(p, F, F, s1, G, G, s2, nullptr, batch, 0, 1, 0, st, &e1);

@@ -176,3 +176,41 @@ def test_k16_other_prime_radices_run_time_modes(r, mode, cuda):
     assert np.array_equal(gp.vec.to_host(h), oplan.poly_mul(x[0], x[1]))
     prod = gp.vec.to_host(gp.vec.mul(xd[0], xd[1], params))
     assert np.array_equal(prod, O.mul(x[0], x[1], r, backend="school"))
+
+
+def test_k8_device_buffers_at_8_byte_offsets(cuda):
+    """Device tensors whose base is only 8-byte aligned cannot be described to
+    the TMA unit (tensor maps need 16 bytes): the same passes then run on the
+    LDG form of the kernel and the poly-multiply keeps its two-kernel middle,
+    with identical results."""
+    import torch
+    import paper_1811_01490_b200 as gp
+    from paper_1811_01490_b200 import _lib
+    lib = _lib.load()
+    params = gp.GfpParams(R8, 8)
+    field = gp.GfpFftField(params, backend="cuda")
+    N = 4096
+    plan = gp.build_plan(field, 16, 3, gp.roots_for(params, N))
+
+    def shifted(t):
+        flat = torch.zeros(t.numel() + 1, dtype=torch.int64, device="cuda")
+        v = flat[1:].view(t.shape)
+        v.copy_(t.view(torch.int64))
+        v = v.view(torch.uint64)
+        assert v.data_ptr() % 16 == 8
+        return v
+
+    f = gp.vec.uniform(N, params, seed=31)
+    g = gp.vec.uniform(N, params, seed=32)
+    want_y = gp.fft_tensor(f, plan)
+    want_h = gp.poly_mul(f, g, plan)
+    fs, gs = shifted(f), shifted(g)
+    before = lib.gfp_tma_pass_launches()
+    out = shifted(torch.zeros_like(f.view(torch.int64)).view(torch.uint64))
+    y = gp.fft_tensor(fs, plan, out=out)
+    assert _eq(y, want_y)
+    h = gp.poly_mul(fs, gs, plan, out=shifted(torch.zeros_like(f.view(torch.int64)).view(torch.uint64)))
+    assert _eq(h, want_h)
+    # aligned output, unaligned inputs: only the first pass falls back
+    assert _eq(gp.fft_tensor(fs, plan), want_y)
+    assert lib.gfp_tma_pass_launches() > before
